@@ -1,0 +1,477 @@
+/*
+ * aw_oracle.c -- plain, slow, obviously-correct CPU ORACLE for the acoustic
+ * wave hot path (arXiv 1906.10811 north star, BASELINE.json:5).
+ *
+ *   *** TEST INFRASTRUCTURE ONLY ***
+ *   Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ *   --impl reference legs may load or execute this file's library.  It shares
+ *   no code, header, table or constant generator with the CUDA product path
+ *   (paper_1906_10811_b200/csrc).  Inputs (m, damp, wavelet, coordinates)
+ *   come from workloads/ which holds none of the method's arithmetic.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, SURVEY = SURVEY.md):
+ *   m*u_tt - Lap(u) + eta*u_t = q      (BASELINE.json:5 north star)
+ *   - FD shortcuts of order = space order, u.dx2 + u.dy2 (+ u.dz2)
+ *        PAPER.md:172 [Background > Devito], :741 [Evaluation > Examined problem]
+ *   - explicit update from solve(eq, u.forward)
+ *   - zero-initialised padding / halo (zero ghosts)  PAPER.md:455-491 [ops_dat creation]
+ *   - divisions hoisted into multiplications          PAPER.md:788-826 [CUDA results]
+ *   - time-buffer rotation t_k = (time + k) mod n     PAPER.md:443 [ops_dat creation]
+ *   The paper never runs the acoustic operator, so the
+ *   discrete readings below are SURVEY.md §8(c) Q1-Q19, listed in DESIGN.md.
+ *
+ * Three modes:
+ *   ORACLE_FP32CANON (0): the parity target.  Exactly this fp32 sequence per
+ *        point (every fl32 one IEEE RN rounding, fmaf correctly rounded; the
+ *        file is compiled with -ffp-contract=off so FMAs appear only where
+ *        written):
+ *          L   = C0 * u_p
+ *          for d = ndim-1 .. 0, j = 1 .. R:   L = fmaf(C[d][j], u_{p-j e_d} + u_{p+j e_d}, L)
+ *          t   = 2*u_p - uprev_p
+ *          w   = fmaf(b_p, L, t)
+ *          oma = 1 - a_p ;  r = oma * uprev_p
+ *          unew_p = fmaf(a_p, w, r)
+ *        then injection  unew[c] = fmaf(s_{s,c}, q[n][s], unew[c])  (corner
+ *        ascending, then source ascending), receivers read u^n before the step.
+ *   ORACLE_FP64CANON (1): the same sequence in fp64 with the SAME fp32-rounded
+ *        coefficient values (isolates fp32 arithmetic noise).
+ *   ORACLE_FP64EXACT (2): the textbook formula in fp64 with fp64 coefficients:
+ *        unew = [dt^2 L + m(2u - uprev) + (eta dt/2) uprev] / (m + eta dt/2)
+ *        injection += w64 dt^2 / den_c * q ; receivers sum w64 * u in fp64.
+ *
+ * Parity pins for each function are in tests/test_oracle_pins.py (P1-P12 of
+ * SURVEY §8(c)); none of them reuses this file's formulas.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_FP32CANON 0
+#define ORACLE_FP64CANON 1
+#define ORACLE_FP64EXACT 2
+
+#define OR_OK 0
+#define OR_EINVAL -1
+#define OR_ENOMEM -2
+
+#define MAXR 8 /* space order <= 16 */
+
+typedef __int128 i128;
+
+static i128 gcd128(i128 a, i128 b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b != 0) { i128 t = a % b; a = b; b = t; }
+    return a;
+}
+
+static i128 fact(int n) {
+    i128 f = 1;
+    for (int i = 2; i <= n; ++i) f *= i;
+    return f;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 1: centred FD weights for the second derivative of
+ * order k = space_order ("space order"):
+ *     c_j = 2 (-1)^{j+1} (m!)^2 / ( j^2 (m-j)! (m+j)! ),  j = 1..m,  m = k/2
+ *     c_0 = -2 sum_j c_j
+ * as exact reduced rationals num[j]/den[j], j = 0..m.
+ * ------------------------------------------------------------------------- */
+int oracle_fd_weights(int space_order, int64_t* num, int64_t* den) {
+    if (space_order < 2 || space_order > 2 * MAXR || (space_order & 1)) return OR_EINVAL;
+    int m = space_order / 2;
+    i128 sn = 0, sd = 1; /* running sum of c_j, j>=1 */
+    for (int j = 1; j <= m; ++j) {
+        i128 n = 2 * fact(m) * fact(m);
+        if (!(j & 1)) n = -n; /* (-1)^{j+1}: + for odd j */
+        i128 d = (i128)j * j * fact(m - j) * fact(m + j);
+        i128 g = gcd128(n, d);
+        n /= g; d /= g;
+        num[j] = (int64_t)n; den[j] = (int64_t)d;
+        /* sn/sd += n/d */
+        i128 nn = sn * d + n * sd, dd = sd * d;
+        g = gcd128(nn, dd);
+        sn = nn / g; sd = dd / g;
+    }
+    /* c_0 = -2 * sum */
+    i128 n0 = -2 * sn, d0 = sd;
+    i128 g = gcd128(n0, d0);
+    num[0] = (int64_t)(n0 / g); den[0] = (int64_t)(d0 / g);
+    return OR_OK;
+}
+
+/* fp64 value of each weight: one correctly-rounded division of the reduced
+ * rational (num, den both < 2^53 for k <= 16). */
+int oracle_fd_weights_f64(int space_order, double* c) {
+    int64_t num[MAXR + 1], den[MAXR + 1];
+    int st = oracle_fd_weights(space_order, num, den);
+    if (st) return st;
+    for (int j = 0; j <= space_order / 2; ++j) c[j] = (double)num[j] / (double)den[j];
+    return OR_OK;
+}
+
+/* Grid spacing h_d = extent_d / (n_d - 1)  (SPEC.md:59-67 convention) */
+static double spacing(const int64_t* shape, const double* extent, int d) {
+    return extent[d] / (double)(shape[d] - 1);
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 2: axis coefficients with division hoisting
+ * ("r0 = 1.0F/(h_y*h_y)"):
+ *     C[d][j] = fl32(c64_j / (h_d*h_d)),   C0 = fl32(sum_d c64_0/(h_d*h_d)) (fp64, axis order)
+ * C is [ndim][MAXR+1]; C[d][0] is set to fl32(c64_0/h_d^2) (unused by the step).
+ * Also returns the fp64 versions (C64, C064) used by mode FP64EXACT.
+ * ------------------------------------------------------------------------- */
+int oracle_axis_coeffs(int ndim, const int64_t* shape, const double* extent, int space_order,
+                       float* C, float* C0, double* C64, double* C064) {
+    double c[MAXR + 1];
+    int st = oracle_fd_weights_f64(space_order, c);
+    if (st) return st;
+    int R = space_order / 2;
+    double s0 = 0.0;
+    for (int d = 0; d < ndim; ++d) {
+        double h = spacing(shape, extent, d);
+        double h2 = h * h;
+        for (int j = 0; j <= MAXR; ++j) {
+            double v = (j <= R) ? c[j] / h2 : 0.0;
+            if (C) C[d * (MAXR + 1) + j] = (float)v;
+            if (C64) C64[d * (MAXR + 1) + j] = v;
+        }
+        s0 = s0 + c[0] / h2;
+    }
+    if (C0) *C0 = (float)s0;
+    if (C064) *C064 = s0;
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 3: point coefficients, per point, from fp32 m, eta
+ * and fp64 dt:   b = fl32(dt^2/m),  den = m + (eta*dt)*0.5,  a = fl32(m/den)
+ * ------------------------------------------------------------------------- */
+static void point_coeffs(float m, float eta, double dt, float* b, float* a, double* den) {
+    double dt2 = dt * dt;
+    double t = (double)eta * dt;
+    double dn = (double)m + t * 0.5;
+    *b = (float)(dt2 / (double)m);
+    *a = (float)((double)m / dn);
+    if (den) *den = dn;
+}
+
+/* ---------------------------------------------------------------------------
+ * Step 4: sparse setup (bit-exact contract, BASELINE.json:5)
+ * For each point and axis d:  p = (x_d - o_d)/h_d (fp64), reject unless
+ * 0 <= p <= n_d-1, i = floor(p), f = p - i.  Corner beta in [0, 2^ndim):
+ * bit d set -> index i_d+1, weight f_d; else index i_d, weight 1-f_d.
+ * Corners with index n_d are skipped (corner = -1, weight 0).
+ * w64 = product of the 1-D weights in axis order.  corner = row-major linear
+ * index over the global grid.  Multilinear interpolation (Q9).
+ * ------------------------------------------------------------------------- */
+int oracle_sparse(int ndim, const int64_t* shape, const double* extent, const double* origin,
+                  int npts, const double* coords, int64_t* corner, double* w64) {
+    int nc = 1 << ndim;
+    for (int s = 0; s < npts; ++s) {
+        int64_t i[3];
+        double f[3];
+        for (int d = 0; d < ndim; ++d) {
+            double o = origin ? origin[d] : 0.0;
+            double h = spacing(shape, extent, d);
+            double p = (coords[s * ndim + d] - o) / h;
+            if (!(p >= 0.0 && p <= (double)(shape[d] - 1))) return OR_EINVAL;
+            double fl = floor(p);
+            i[d] = (int64_t)fl;
+            f[d] = p - fl;
+        }
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t lin = 0;
+            double w = 1.0;
+            int skip = 0;
+            for (int d = 0; d < ndim; ++d) {
+                int up = (beta >> d) & 1;
+                int64_t idx = i[d] + up;
+                if (idx >= shape[d]) skip = 1;
+                double wd = up ? f[d] : (1.0 - f[d]);
+                w = (d == 0) ? wd : w * wd;
+                lin = lin * shape[d] + idx;
+            }
+            corner[s * nc + beta] = skip ? -1 : lin;
+            w64[s * nc + beta] = skip ? 0.0 : w;
+        }
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* zero-ghost access (Q3: u == 0 outside the domain)        */
+static inline int inside(int ndim, const int64_t* shape, const int64_t* idx) {
+    for (int d = 0; d < ndim; ++d)
+        if (idx[d] < 0 || idx[d] >= shape[d]) return 0;
+    return 1;
+}
+static inline int64_t lin_index(int ndim, const int64_t* shape, const int64_t* idx) {
+    int64_t l = 0;
+    for (int d = 0; d < ndim; ++d) l = l * shape[d] + idx[d];
+    return l;
+}
+
+typedef struct {
+    int64_t key;   /* corner linear index */
+    int src;       /* source index */
+    int beta;
+} inj_entry;
+
+static int inj_cmp(const void* x, const void* y) {
+    const inj_entry* a = (const inj_entry*)x;
+    const inj_entry* b = (const inj_entry*)y;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    if (a->src != b->src) return a->src < b->src ? -1 : 1;
+    return a->beta - b->beta;
+}
+
+/* ---------------------------------------------------------------------------
+ * oracle_run: advance nt steps.
+ *   shape/extent/origin : grid (origin may be NULL = 0)
+ *   m, damp             : fp32 [N] slowness^2 and eta (damp may be NULL = 0)
+ *   dt                  : time step
+ *   n0                  : global index of the first step (wavelet row n0)
+ *   ns, src_coords      : [ns][ndim]; wavelet [nt_total rows >= n0+nt][ns] fp32
+ *   nr, rec_coords      : [nr][ndim]; rec_out [nt][nr] (float for mode 0, double else)
+ *   u_cur, u_prev       : in/out level n0 and n0-1 (float for mode 0, double else),
+ *                         on return levels n0+nt and n0+nt-1.
+ *   nthreads            : OpenMP threads (<=0: runtime default)
+ * Three logical time slots rotated as t_k = (n + k) mod 3.
+ * ------------------------------------------------------------------------- */
+int oracle_run(int mode, int ndim, const int64_t* shape, const double* extent, const double* origin,
+               int space_order, const float* m, const float* damp, double dt, int n0, int nt,
+               int ns, const double* src_coords, const float* wavelet,
+               int nr, const double* rec_coords, void* rec_out,
+               void* u_cur, void* u_prev, int nthreads) {
+    if (ndim < 2 || ndim > 3) return OR_EINVAL;
+    if (space_order < 2 || space_order > 2 * MAXR || (space_order & 1)) return OR_EINVAL;
+    if (mode < 0 || mode > 2 || nt < 0) return OR_EINVAL;
+    const int R = space_order / 2;
+    const int nc = 1 << ndim;
+    int64_t N = 1;
+    for (int d = 0; d < ndim; ++d) {
+        if (shape[d] < R + 1) return OR_EINVAL;
+        N *= shape[d];
+    }
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+
+    /* Step 2: axis coefficients */
+    float C[3 * (MAXR + 1)], C0;
+    double C64[3 * (MAXR + 1)], C064;
+    oracle_axis_coeffs(ndim, shape, extent, space_order, C, &C0, C64, &C064);
+
+    /* Step 3: point coefficients */
+    float* b = (float*)malloc(sizeof(float) * N);
+    float* a = (float*)malloc(sizeof(float) * N);
+    if (!b || !a) { free(b); free(a); return OR_ENOMEM; }
+    for (int64_t p = 0; p < N; ++p) {
+        if (!(m[p] > 0.0f) || !isfinite(m[p])) { free(b); free(a); return OR_EINVAL; }
+        float eta = damp ? damp[p] : 0.0f;
+        if (!(eta >= 0.0f)) { free(b); free(a); return OR_EINVAL; }
+        point_coeffs(m[p], eta, dt, &b[p], &a[p], NULL);
+    }
+    const double dt2 = dt * dt;
+
+    /* Step 4: sparse setup */
+    int64_t* scorner = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ns > 0 ? ns : 1) * nc);
+    double* sw64 = (double*)malloc(sizeof(double) * (size_t)(ns > 0 ? ns : 1) * nc);
+    int64_t* rcorner = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1) * nc);
+    double* rw64 = (double*)malloc(sizeof(double) * (size_t)(nr > 0 ? nr : 1) * nc);
+    inj_entry* inj = (inj_entry*)malloc(sizeof(inj_entry) * (size_t)(ns > 0 ? ns : 1) * nc);
+    float* s32 = (float*)malloc(sizeof(float) * (size_t)(ns > 0 ? ns : 1) * nc);
+    double* s64 = (double*)malloc(sizeof(double) * (size_t)(ns > 0 ? ns : 1) * nc);
+    int st = OR_OK;
+    if (!scorner || !sw64 || !rcorner || !rw64 || !inj || !s32 || !s64) { st = OR_ENOMEM; goto done_sparse; }
+    if (ns > 0 && oracle_sparse(ndim, shape, extent, origin, ns, src_coords, scorner, sw64)) { st = OR_EINVAL; goto done_sparse; }
+    if (nr > 0 && oracle_sparse(ndim, shape, extent, origin, nr, rec_coords, rcorner, rw64)) { st = OR_EINVAL; goto done_sparse; }
+    int ninj = 0;
+    for (int s = 0; s < ns; ++s)
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t c = scorner[s * nc + beta];
+            if (c < 0) continue;
+            float eta = damp ? damp[c] : 0.0f;
+            double den;
+            float bb, aa;
+            point_coeffs(m[c], eta, dt, &bb, &aa, &den);
+            s32[s * nc + beta] = (float)((sw64[s * nc + beta] * dt2) / den);
+            s64[s * nc + beta] = sw64[s * nc + beta] * dt2 / den;
+            inj[ninj].key = c; inj[ninj].src = s; inj[ninj].beta = beta;
+            ++ninj;
+        }
+    qsort(inj, (size_t)ninj, sizeof(inj_entry), inj_cmp); /* CSR order: corner, then source (Q11) */
+
+    /* Three logical time slots, rotated t_k = (n+k) mod 3. */
+    size_t esz = (mode == ORACLE_FP32CANON) ? sizeof(float) : sizeof(double);
+    void* slot[3];
+    slot[0] = malloc(esz * N); slot[1] = malloc(esz * N); slot[2] = malloc(esz * N);
+    if (!slot[0] || !slot[1] || !slot[2]) { st = OR_ENOMEM; free(slot[0]); free(slot[1]); free(slot[2]); goto done_sparse; }
+    /* level n lives in slot (n mod 3); n counted from 1 here so level n0-1 -> slot 0 */
+    memcpy(slot[1], u_cur, esz * N);   /* level n0   -> slot (1) */
+    memcpy(slot[0], u_prev, esz * N);  /* level n0-1 -> slot (0) */
+
+    for (int step = 0; step < nt; ++step) {
+        int n = n0 + step;
+        /* local counter k = step+1 is level n; slots: prev (k-1)%3, cur k%3, next (k+1)%3 */
+        int k = step + 1;
+        void* vprev = slot[(k - 1) % 3];
+        void* vcur = slot[k % 3];
+        void* vnext = slot[(k + 1) % 3];
+
+        /* 6.1 receivers read u^n (Q8) */
+        for (int r = 0; r < nr; ++r) {
+            if (mode == ORACLE_FP32CANON) {
+                const float* u = (const float*)vcur;
+                float acc = 0.0f;
+                for (int beta = 0; beta < nc; ++beta) {
+                    int64_t c = rcorner[r * nc + beta];
+                    if (c < 0) continue;
+                    acc = fmaf((float)rw64[r * nc + beta], u[c], acc);
+                }
+                ((float*)rec_out)[(int64_t)step * nr + r] = acc;
+            } else if (mode == ORACLE_FP64CANON) {
+                const double* u = (const double*)vcur;
+                double acc = 0.0;
+                for (int beta = 0; beta < nc; ++beta) {
+                    int64_t c = rcorner[r * nc + beta];
+                    if (c < 0) continue;
+                    acc = fma((double)(float)rw64[r * nc + beta], u[c], acc);
+                }
+                ((double*)rec_out)[(int64_t)step * nr + r] = acc;
+            } else {
+                const double* u = (const double*)vcur;
+                double acc = 0.0;
+                for (int beta = 0; beta < nc; ++beta) {
+                    int64_t c = rcorner[r * nc + beta];
+                    if (c < 0) continue;
+                    acc += rw64[r * nc + beta] * u[c];
+                }
+                ((double*)rec_out)[(int64_t)step * nr + r] = acc;
+            }
+        }
+
+        /* 6.2 stencil + damped leapfrog update at every domain point (Q4) */
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < N; ++p) {
+            int64_t idx[3], q[3];
+            int64_t rem = p;
+            for (int d = ndim - 1; d >= 0; --d) { idx[d] = rem % shape[d]; rem /= shape[d]; }
+            if (mode == ORACLE_FP32CANON) {
+                const float* u = (const float*)vcur;
+                const float* um1 = (const float*)vprev;
+                float L = C0 * u[p];
+                for (int d = ndim - 1; d >= 0; --d) {
+                    for (int j = 1; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] - j;
+                        float lo = inside(ndim, shape, q) ? u[lin_index(ndim, shape, q)] : 0.0f;
+                        q[d] = idx[d] + j;
+                        float hi = inside(ndim, shape, q) ? u[lin_index(ndim, shape, q)] : 0.0f;
+                        float pair = lo + hi;
+                        L = fmaf(C[d * (MAXR + 1) + j], pair, L);
+                    }
+                }
+                float t = 2.0f * u[p] - um1[p];
+                float w = fmaf(b[p], L, t);
+                float oma = 1.0f - a[p];
+                float rr = oma * um1[p];
+                ((float*)vnext)[p] = fmaf(a[p], w, rr);
+            } else if (mode == ORACLE_FP64CANON) {
+                const double* u = (const double*)vcur;
+                const double* um1 = (const double*)vprev;
+                double L = (double)C0 * u[p];
+                for (int d = ndim - 1; d >= 0; --d) {
+                    for (int j = 1; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] - j;
+                        double lo = inside(ndim, shape, q) ? u[lin_index(ndim, shape, q)] : 0.0;
+                        q[d] = idx[d] + j;
+                        double hi = inside(ndim, shape, q) ? u[lin_index(ndim, shape, q)] : 0.0;
+                        L = fma((double)C[d * (MAXR + 1) + j], lo + hi, L);
+                    }
+                }
+                double t = 2.0 * u[p] - um1[p];
+                double w = fma((double)b[p], L, t);
+                double rr = (1.0 - (double)a[p]) * um1[p];
+                ((double*)vnext)[p] = fma((double)a[p], w, rr);
+            } else {
+                /* textbook: L = sum_d sum_{j=-R..R} c_|j|/h_d^2 u(p + j e_d) */
+                const double* u = (const double*)vcur;
+                const double* um1 = (const double*)vprev;
+                double L = 0.0;
+                for (int d = 0; d < ndim; ++d) {
+                    for (int j = -R; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] + j;
+                        double v = inside(ndim, shape, q) ? u[lin_index(ndim, shape, q)] : 0.0;
+                        L += C64[d * (MAXR + 1) + (j < 0 ? -j : j)] * v;
+                    }
+                }
+                double mm = (double)m[p];
+                double he = (damp ? (double)damp[p] : 0.0) * dt * 0.5;
+                ((double*)vnext)[p] = (dt2 * L + mm * (2.0 * u[p] - um1[p]) + he * um1[p]) / (mm + he);
+            }
+        }
+
+        /* 6.3 injection into u^{n+1}: corner ascending, then source ascending (Q6, Q11) */
+        for (int e = 0; e < ninj; ++e) {
+            int s = inj[e].src, beta = inj[e].beta;
+            int64_t c = inj[e].key;
+            float q32 = wavelet[(int64_t)n * ns + s];
+            if (mode == ORACLE_FP32CANON) {
+                float* un = (float*)vnext;
+                un[c] = fmaf(s32[s * nc + beta], q32, un[c]);
+            } else if (mode == ORACLE_FP64CANON) {
+                double* un = (double*)vnext;
+                un[c] = fma((double)s32[s * nc + beta], (double)q32, un[c]);
+            } else {
+                double* un = (double*)vnext;
+                un[c] += s64[s * nc + beta] * (double)q32;
+            }
+        }
+        /* 6.4 rotate: implicit in the slot index (k+1)%3 */
+    }
+    /* after nt steps the newest level n0+nt lives in slot (nt+1)%3, the previous in nt%3 */
+    memcpy(u_cur, slot[(nt + 1) % 3], esz * N);
+    memcpy(u_prev, slot[nt % 3], esz * N);
+    free(slot[0]); free(slot[1]); free(slot[2]);
+done_sparse:
+    free(scorner); free(sw64); free(rcorner); free(rw64); free(inj); free(s32); free(s64);
+    free(b); free(a);
+    return st;
+}
+
+/* Export the point coefficients for one (m, eta, dt) for tests. */
+void oracle_point_coeffs(int64_t n, const float* m, const float* damp, double dt, float* b, float* a) {
+    for (int64_t p = 0; p < n; ++p) point_coeffs(m[p], damp ? damp[p] : 0.0f, dt, &b[p], &a[p], NULL);
+}
+
+/* Source scales s = fl32((w64*dt^2)/den_c) for tests of the sparse contract. */
+int oracle_source_scales(int ndim, const int64_t* shape, const double* extent, const double* origin,
+                         const float* m, const float* damp, double dt, int ns, const double* coords,
+                         int64_t* corner, float* s) {
+    int nc = 1 << ndim;
+    double* w = (double*)malloc(sizeof(double) * (size_t)(ns > 0 ? ns : 1) * nc);
+    if (!w) return OR_ENOMEM;
+    int st = oracle_sparse(ndim, shape, extent, origin, ns, coords, corner, w);
+    if (st == OR_OK) {
+        for (int i = 0; i < ns * nc; ++i) {
+            if (corner[i] < 0) { s[i] = 0.0f; continue; }
+            double den; float bb, aa;
+            point_coeffs(m[corner[i]], damp ? damp[corner[i]] : 0.0f, dt, &bb, &aa, &den);
+            s[i] = (float)((w[i] * (dt * dt)) / den);
+        }
+    }
+    free(w);
+    return st;
+}
