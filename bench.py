@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- Gpts/s of the B200 acoustic-wave hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl aw|reference] [--workload C3|C5|C2|C1]
+
+A bench "step" is one pass of the whole hot path over one batch of synthetic
+input: reset, set_model (-> b, a coefficient precompute at run), sparse
+setup of sources and receivers, `nt` leapfrog time steps (stencil + update +
+injection + receivers [+ halo exchange]), and the trace readback.  At N=1 the
+workload is config C3 (512^3, space order 8, 1000 time steps, random smooth
+model, nbl 32): BASELINE.json's 1-GPU roofline run.  At N>1 each GPU owns a
+512^3 slab of a (512N, 512, 512) grid (weak scaling; halo exchange fused
+into the stencil over NVLink peer memory).
+
+value  = grid-point updates / s over the K timed steps (CUDA events on the
+         launching stream, inputs resident in HBM, max over ranks)
+e2e    = the same metric through the C ABI with pinned HOST inputs/outputs
+         (model, wavelet H2D and trace D2H inside the timed region)
+roofline: stencil kernel, 16 algorithmic B/point-update over
+         its event-timed average launch duration vs MEASURED_PEAKS.json.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_STRICT = 16  # algorithmic bytes per point update: read u^n, u^{n-1}, b; write u^{n+1}
+METRIC = "Gpts/s (grid-point updates/s) and % of HBM roofline at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="aw", choices=["aw", "reference"])
+    ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--nt", type=int, default=None, help="override time steps per bench step")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "v1", "stream"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle time steps in the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.out = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.out,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.out.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload (seeded synthetic inputs; recipe in workloads/ and DESIGN.md §5)
+# ---------------------------------------------------------------------------
+def workload_spec(name, world):
+    import workloads as W
+    if name == "C3":
+        N = world
+        shape = (512 * N, 512, 512)
+        base = W.c3(with_arrays=False)
+        src = np.array([[base.src_coords[0][0] + 5120.0 * i, *base.src_coords[0][1:]] for i in range(N)])
+        rec = base.rec_coords
+        if N > 1:
+            rec = np.concatenate([rec, np.array([[10.0 * r, 2555.3, 2554.7] for r in range(shape[0])])])
+        return dict(name="C3" if N == 1 else f"C3-weak(N={N})", shape=shape, so=8, nt=base.nt, dt=base.dt,
+                    f0=base.f0, nbl=32, model="random_smooth", src=src, rec=rec)
+    if name == "C5":
+        base = W.c5(N=world, with_arrays=False)
+        return dict(name=f"C5(N={world})", shape=base.shape, so=16, nt=base.nt, dt=base.dt, f0=base.f0, nbl=32,
+                    model="random_smooth", src=base.src_coords, rec=base.rec_coords)
+    if name == "C2":
+        base = W.c2()
+        return dict(name="C2", shape=base.shape, so=4, nt=base.nt, dt=base.dt, f0=base.f0, nbl=16,
+                    model="two_layer", src=base.src_coords, rec=base.rec_coords, arrays=base)
+    base = W.c1()
+    return dict(name="C1", shape=base.shape, so=2, nt=base.nt, dt=base.dt, f0=base.f0, nbl=0, model="constant",
+                src=base.src_coords, rec=base.rec_coords, arrays=base)
+
+
+def local_model(spec, z0, nz, device):
+    """m, eta for planes [z0, z0+nz) as torch tensors on `device`."""
+    import torch
+    import workloads as W
+    if "arrays" in spec:
+        a = spec["arrays"]
+        m = torch.from_numpy(a.m[z0:z0 + nz].copy()).to(device)
+        d = None if a.damp is None else torch.from_numpy(a.damp[z0:z0 + nz].copy()).to(device)
+        return m, d
+    m = W.random_smooth_m(spec["shape"], z0=z0, nz=nz, device=str(device))
+    d = torch.from_numpy(W.damping_profile(spec["shape"], spec["nbl"], z0=z0, nz=nz)).to(device)
+    return m, d
+
+
+# ---------------------------------------------------------------------------
+# the reference arm / cpu baseline: the oracle as it stands, on a bounded sample
+# ---------------------------------------------------------------------------
+def oracle_sample(spec, nsteps):
+    import oracle
+    import workloads as W
+    shape = spec["shape"]
+    if "arrays" in spec:
+        m, damp = spec["arrays"].m, spec["arrays"].damp
+    else:
+        m = W.random_smooth_m(shape)
+        damp = W.damping_profile(shape, spec["nbl"])
+    wav = W.ricker(nsteps, spec["dt"], spec["f0"], ns=len(spec["src"]))
+    extent = [10.0 * (n - 1) for n in shape]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.run(oracle.FP32CANON, shape, extent, spec["so"], m, spec["dt"], nsteps, damp=damp, src_coords=spec["src"],
+               wavelet=wav, rec_coords=spec["rec"], nthreads=threads)
+    t = time.perf_counter() - t0
+    pts = float(np.prod(shape)) * nsteps
+    return pts / t / 1e9, t, threads
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (CPU) on the same workload, metric and unit."""
+    if rank != 0:
+        return
+    spec = workload_spec(args.workload, 1 if world == 1 else world)
+    nsteps = args.cpu_steps
+    vals, secs = [], []
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_sample(spec, 1)
+    for _ in range(args.steps):
+        v, t, threads = oracle_sample(spec, nsteps)
+        vals.append(v)
+        secs.append(t)
+    total_pts = float(np.prod(spec["shape"])) * nsteps * args.steps
+    value = total_pts / sum(secs) / 1e9
+    sample = (f"{spec['name']} grid {spec['shape']}, so {spec['so']}, {nsteps} of {spec['nt']} time steps per "
+              f"bench step (whole oracle_run call incl. its coefficient setup)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gpts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": spec["name"], "shape": list(spec["shape"]), "space_order": spec["so"],
+                       "time_steps": nsteps},
+            "cpu_baseline": {"value": round(value, 4), "unit": "Gpts/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.warmup < 3:
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+        sys.exit(2)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1906_10811_b200 import build as awbuild
+    if rank == 0 or world == 1:
+        awbuild.build()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    import paper_1906_10811_b200 as aw
+
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    spec = workload_spec(args.workload, world)
+    nt = args.nt or spec["nt"]
+    shape = spec["shape"]
+    extent = [10.0 * (n - 1) for n in shape]
+    stream = torch.cuda.current_stream()
+
+    g = aw.Grid(shape, extent, spec["so"], rank=rank, world=world, device=local, stream=stream)
+    if args.kernel != "auto":
+        g.set_option(aw.AW_OPT_KERNEL, {"v1": aw.AW_KERNEL_V1, "stream": aw.AW_KERNEL_STREAM}[args.kernel])
+    if world > 1:
+        rec_bytes = g.team_export()
+        t = torch.frombuffer(bytearray(rec_bytes), dtype=torch.uint8).to(device)
+        allt = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        g.team_connect(b"".join(bytes(x.cpu().numpy().tobytes()) for x in allt))
+        dist.barrier()
+
+    import workloads as W
+    m_dev, d_dev = local_model(spec, g.z0, g.nz, device)
+    wav = W.ricker(nt, spec["dt"], spec["f0"], ns=len(spec["src"]))
+    wav_dev = torch.from_numpy(wav).to(device)
+    nr = len(spec["rec"])
+    traces_dev = torch.zeros((nt, nr), dtype=torch.float32, device=device)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def one_step(m, d, wv, traces):
+        barrier()  # team calls: neighbours finished the previous run before anyone resets
+        g.reset()
+        g.set_model(m, d, aw.AW_LOCAL)
+        g.add_sources(spec["src"], wv)
+        g.add_receivers(spec["rec"], nt)
+        barrier()
+        g.run(nt, spec["dt"])
+        g.read_receivers(out=traces)
+
+    for _ in range(args.warmup):
+        one_step(m_dev, d_dev, wav_dev, traces_dev)
+
+    # ---- timed region: K steps, inputs resident in HBM ----
+    g.set_option(aw.AW_OPT_TIMING, 1)  # per-launch CUDA events around the stencil kernel
+    clocks = Clocks(local)
+    launches0 = g.stats()["launches_total"]
+    torch.cuda.synchronize()
+    barrier()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    ms_stencil, n_stencil = 0.0, 0
+    for _ in range(args.steps):
+        one_step(m_dev, d_dev, wav_dev, traces_dev)
+        st = g.stats()
+        ms_stencil += st["ms_stencil"]
+        n_stencil += st["n_stencil"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = g.stats()["launches_total"] - launches0
+    st = g.stats()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_pts = float(np.prod(shape)) * nt * args.steps
+    value = total_pts / (ms * 1e-3) / 1e9
+
+    # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        g.set_option(aw.AW_OPT_TIMING, 0)
+        m_h = m_dev.cpu().pin_memory()
+        d_h = d_dev.cpu().pin_memory() if d_dev is not None else None
+        wav_h = torch.from_numpy(wav).pin_memory()
+        tr_h = torch.zeros((nt, nr), dtype=torch.float32).pin_memory()
+        one_step(m_h, d_h, wav_h, tr_h)  # warm the host path
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step(m_h, d_h, wav_h, tr_h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = m_h.numel() * 4 + (d_h.numel() * 4 if d_h is not None else 0) + wav_h.numel() * 4 \
+            + spec["src"].size * 8 + spec["rec"].size * 8
+        e2e = {"value": round(total_pts / (ems * 1e-3) / 1e9, 3), "unit": "Gpts/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(tr_h.numel() * 4), "ms_per_step": round(ems / args.steps, 3)}
+
+    # ---- roofline of the dominant kernel (stencil) ----
+    peak, peak_src = load_peaks()
+    pts_local = float(g.nz) * float(np.prod(shape[1:]))
+    avg_ms = ms_stencil / max(1, n_stencil)
+    achieved = B_STRICT * pts_local / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    kname = "stream" if st["kernel"] == aw.AW_KERNEL_STREAM else "v1"
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        ent = tj.get(f"{spec['name']}:{kname}")
+        if ent:
+            traffic = ent.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+                "kernel": f"stencil_{kname}", "bytes_per_point": B_STRICT, "peak_source": peak_src,
+                "stencil_ms_avg": round(avg_ms, 4), "stencil_share_of_step": round(ms_stencil / ms, 4) if ms else None}
+
+    # ---- cpu baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, t, threads = oracle_sample(spec, args.cpu_steps)
+        cpu = {"value": round(v, 5), "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+               "sample": f"{spec['name']} grid {list(shape)}, so {spec['so']}, {args.cpu_steps} time steps "
+                         f"(whole oracle_run call, {t:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": spec["name"], "shape": list(shape), "space_order": spec["so"],
+                           "time_steps": nt, "dt_ms": spec["dt"], "model": spec["model"], "nbl": spec["nbl"],
+                           "sources": len(spec["src"]), "receivers": nr, "parallelism": f"slab{world}",
+                           "l2": "inputs larger than L2 (working set %.1f GiB)" % (
+                               pts_local * 4 * (4 + (1 if d_dev is not None else 0) * 2) / 2 ** 30)},
+                "hbm_pct_strict": round(100 * value * B_STRICT / world / peak, 2),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,229 @@
+/*
+ * aw.h -- acoustic wave propagation on B200 (sm_100a): the C-ABI boundary of
+ * the hot path named by BASELINE.json:5 (north star) for arXiv 1906.10811.
+ *
+ *   m * u_tt - Lap(u) + eta * u_t = q          on a structured 2D/3D grid
+ *
+ * discretised as a space-order-k star stencil ("FD shortcuts",
+ * :741 "u.dx2 + u.dy2", :746 order = space order) with the explicit update
+ * obtained from solve(eq, u.forward), divisions hoisted
+ * into precomputed coefficients (PAPER.md:788-826 [Evaluation > CUDA results]),
+ * zero-initialised halos, time levels rotated
+ * t_k = (time+k) mod n, and sparse Ricker-source injection and
+ * receiver interpolation inside the time loop -- the part OPS could not
+ * offload.  The exact per-point fp32 operation sequence is
+ * SURVEY.md §8(c) steps 1-6 (the "canonical" order), restated in DESIGN.md §2.
+ *
+ * Conventions
+ *  - Arrays are C-contiguous with shape (n0, n1[, n2]); axis ndim-1 is
+ *    contiguous ("x"), axis 0 is the slowest ("z"), the streaming axis and the
+ *    slab (multi-GPU) axis.  Coordinates are given in the same axis order.
+ *  - Spacing h_d = extent_d / (n_d - 1); origin defaults to 0.
+ *  - Array arguments marked [H|D] may be host or device pointers (detected
+ *    with cudaPointerGetAttributes; device pointers must be on the grid's
+ *    device).  [H] = host only.  All inputs are BORROWED for the duration of
+ *    the call and copied; outputs are caller-allocated with the sizes stated.
+ *  - Every call returns aw_status; aw_last_error() gives a thread-local text.
+ *    Validation errors (AW_EINVAL / AW_EUNSUPPORTED) leave the handle
+ *    unchanged.  AW_ECUDA is sticky: the handle is poisoned and every later
+ *    call except aw_grid_destroy returns AW_ESTATE.
+ *  - Calls on one handle are not thread-safe (concurrent reads are
+ *    safe, writes require external exclusivity).  All calls are synchronous
+ *    with respect to the handle's stream except where stated.
+ *  - There is no CPU fallback: without a usable CUDA device aw_grid_create
+ *    returns AW_ECUDA.
+ */
+#ifndef AW_H
+#define AW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define AW_ABI_VERSION 1
+
+typedef struct aw_grid aw_grid; /* opaque; created by aw_grid_create, freed by aw_grid_destroy */
+
+typedef enum {
+    AW_OK = 0,
+    AW_EINVAL = -1,        /* bad argument (shape, order, coordinate outside the grid, ...) */
+    AW_ENOMEM = -2,        /* device or host allocation failed */
+    AW_ECUDA = -3,         /* CUDA runtime/launch error (sticky) */
+    AW_ENCCL = -4,         /* reserved (peer-memory team setup failure uses AW_ECUDA) */
+    AW_ESTATE = -5,        /* call not valid in the current state (poisoned handle, no model, ...) */
+    AW_EUNSUPPORTED = -6,  /* valid request the library does not implement (e.g. ndim 1) */
+    AW_ENONFINITE = -7     /* NaN/Inf appeared in the receivers or the final wavefield */
+} aw_status;
+
+/* layout of array arguments for multi-rank handles */
+enum { AW_GLOBAL = 0 /* array covers the whole global grid */, AW_LOCAL = 1 /* this rank's slab only */ };
+
+/* stencil kernel selection (aw_set_option AW_OPT_KERNEL) */
+enum { AW_KERNEL_AUTO = 0, AW_KERNEL_V1 = 1 /* one thread per point, reference-grade */,
+       AW_KERNEL_STREAM = 2 /* 2.5D z-streaming TMA kernel (3D) */ };
+
+/* options */
+enum {
+    AW_OPT_KERNEL = 1,      /* value: AW_KERNEL_* */
+    AW_OPT_TIMING = 2,      /* value 1: time every stencil launch with CUDA events (no graphs) */
+    AW_OPT_GRAPH_STEPS = 3, /* value G >= 0: steps per captured CUDA graph (0 = no graphs) */
+    AW_OPT_CHECK_FINITE = 4 /* value 0/1 (default 1): aw_run checks traces + final field */
+};
+
+/* multi-rank description: one process (or virtual rank) per slab of axis 0 */
+typedef struct {
+    int rank;       /* 0 <= rank < world */
+    int world;      /* number of slabs along axis 0 (1 = single GPU) */
+    int device;     /* CUDA device ordinal to use (-1 = current device) */
+    void* stream;   /* cudaStream_t to launch on (NULL = library-owned stream) */
+} aw_dist;
+
+/*
+ * aw_grid_create -- allocate a zero-initialised grid handle (PAPER.md:455-491
+ * zero padding).
+ *   ndim         2 or 3 (1 -> AW_EUNSUPPORTED)
+ *   shape[ndim]  global points per axis; n_d >= k/2 + 1
+ *   extent[ndim] physical length per axis, > 0 (h_d = extent_d/(n_d-1))
+ *   origin[ndim] physical coordinate of node 0 (NULL = zeros)
+ *   space_order  k: even, 2..16
+ *   dist         NULL = one slab on the current device; otherwise the slab
+ *                [z0, z0+nz) of axis 0 owned by dist->rank (nearly equal split)
+ * Device memory: 2 wavefield levels with k/2 halo planes on each side of
+ * axis 0 plus b, a, m, eta per owned point (fp32, x pitch padded to 128 B).
+ */
+aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const double* extent,
+                         const double* origin, int space_order, const aw_dist* dist);
+
+/* NULL-safe; never fails.  Must not be called while another rank of a team still runs. */
+void aw_grid_destroy(aw_grid* g);
+
+/* This handle's slab of axis 0: planes [*z0, *z0 + *nz). */
+aw_status aw_local_extent(const aw_grid* g, int64_t* z0, int64_t* nz);
+
+/*
+ * aw_set_model -- slowness squared m = 1/v^2 (> 0, finite) and damping eta
+ * (>= 0, finite; NULL = 0 everywhere), fp32 [H|D], shape = global grid
+ * (AW_GLOBAL) or this rank's slab (AW_LOCAL).  The dt-dependent coefficients
+ * b = fl32(dt^2/m), a = fl32(m/(m + eta dt/2)) (the paper's
+ * division hoisting PAPER.md:788-792) are (re)computed on the device at the
+ * next aw_run.  Invalid values -> AW_EINVAL (checked on the device).
+ */
+aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout);
+
+/*
+ * aw_add_sources -- replace the point sources.
+ *   coords [ns][ndim] fp64 [H]: physical coordinates inside the closed grid box
+ *   wavelet [nt_max][ns] fp32 [H|D]: row n = source amplitudes q at step n
+ * Injection at step n adds s * q[n][s] to u^{n+1} at each of the 2^ndim
+ * multilinear corners, s = fl32(w*dt^2/(m_c + eta_c dt/2)),
+ * corners ascending then sources ascending (Q11).  ns = 0 removes all sources.
+ * A coordinate outside [o, o+(n-1)h] on any axis -> AW_EINVAL.
+ */
+aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, const float* wavelet);
+
+/*
+ * aw_add_receivers -- replace the receivers; traces are recorded from u^n
+ * (before step n) for steps 0..nt_max-1 (Q8).  coords [nr][ndim] fp64 [H].
+ * Corner indices and fp32 weights are computed on the host in fp64 exactly as
+ * SURVEY §8(c).4 (bit-exact contract).  Clears previously recorded traces.
+ */
+aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max);
+
+/*
+ * aw_set_wavefield -- initial conditions / restart: u_cur = u^{n}, u_prev =
+ * u^{n-1} (fp32 [H|D], NULL = zeros) for the current step counter.
+ */
+aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, int layout);
+
+/*
+ * aw_run -- advance nt >= 0 steps from the current state with time step dt
+ * (> 0, finite).  dt is fixed by the first run until aw_reset (a different
+ * dt -> AW_EINVAL).  Needs a model (AW_ESTATE otherwise); the wavelet and
+ * trace buffers must cover steps_done + nt (AW_EINVAL otherwise).  For a team
+ * (world > 1) every rank calls aw_run collectively.  Returns after the work
+ * completed on the handle's stream; AW_ENONFINITE if NaN/Inf appeared.
+ */
+aw_status aw_run(aw_grid* g, int nt, double dt);
+
+/* Zero both wavefield levels and the traces, reset the step counter and dt. */
+aw_status aw_reset(aw_grid* g);
+
+/* Number of steps taken since create/reset. */
+int64_t aw_steps_done(const aw_grid* g);
+
+/*
+ * aw_read_wavefield -- copy u^{n} (which = 0, the newest level) or u^{n-1}
+ * (which = 1) into out (fp32 [H|D], dense, global or local layout; a rank
+ * asked for AW_GLOBAL writes only its own planes of the global array).
+ */
+aw_status aw_read_wavefield(aw_grid* g, int which, float* out, int layout);
+
+/*
+ * aw_read_receivers -- traces [steps_done][nr] fp32 [H|D], row = step.
+ * In a team each rank returns its owned receivers and zeros elsewhere; the
+ * sum over ranks is the global trace set (disjoint supports, exact).
+ */
+aw_status aw_read_receivers(aw_grid* g, float* out);
+
+/*
+ * aw_debug_sparse -- test hook: for which = 0 (sources) / 1 (receivers), the
+ * global row-major corner indices [n][2^ndim] (-1 = skipped corner) and the
+ * fp32 weights (receivers) or source scales (sources; valid after a run).
+ * [H] outputs.
+ */
+aw_status aw_debug_sparse(const aw_grid* g, int which, int64_t* corner_lin, float* w);
+
+typedef struct {
+    double ms_total;      /* wall time of the last aw_run on the stream (CUDA events) */
+    double ms_stencil;    /* sum of stencil-kernel durations (AW_OPT_TIMING=1, else -1) */
+    int64_t n_stencil;    /* stencil launches timed */
+    int64_t launches;     /* kernels launched by the last aw_run (all kinds) */
+    double gpts;          /* point updates / s of the last run (global points, this rank's time) */
+    int64_t points;       /* owned points per step */
+    int kernel;           /* AW_KERNEL_* actually used */
+    int eta_tiles;        /* percent of stream tiles that read `a` (damping present) */
+    int64_t launches_total; /* kernels launched by this handle since creation (all calls) */
+} aw_run_stats;
+
+aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out);
+
+aw_status aw_set_option(aw_grid* g, int option, int64_t value);
+
+/* Leapfrog stability limit 2/(vmax sqrt(sum_d sum_j |c_j|/h_d^2)). */
+double aw_critical_dt(int ndim, const double* spacing, int space_order, double vmax);
+
+const char* aw_last_error(void);
+int aw_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Multi-slab teams: slabs along axis 0, per-step k/2-plane
+ * halo exchange fused into the stencil kernel as direct stores into the
+ * neighbours' halo planes over NVLink peer memory, with a device flag
+ * handshake per step (no separate copy kernel, no host round trip).
+ * ------------------------------------------------------------------------ */
+
+/* Bytes of the opaque export record of one rank (cudaIpc handles + offsets). */
+size_t aw_team_export_size(void);
+/* Write this rank's export record into out[aw_team_export_size()]. */
+aw_status aw_team_export(aw_grid* g, void* out);
+/* Connect to the neighbours from all ranks' records, concatenated in rank
+ * order (world * aw_team_export_size() bytes, [H]).  Collective. */
+aw_status aw_team_connect(aw_grid* g, const void* all_records);
+/* Virtual ranks in one process (tests on one GPU): grids[r] has rank r. */
+aw_status aw_team_connect_local(aw_grid** grids, int world);
+/* Drive virtual ranks step by step on their streams (one process). */
+aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* AW_H */

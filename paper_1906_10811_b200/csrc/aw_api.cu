@@ -1,0 +1,1216 @@
+// aw_api.cu -- host runtime of libaw: the C-ABI of include/aw.h.
+//
+// Validation, device layout, sparse setup (fp64 index/weight computation,
+// SURVEY.md §8(c).4), FD-weight and axis-coefficient tables (§8(c).1-2), the
+// on-device time loop (CUDA graphs of G steps or timed direct launches), the
+// multi-slab team (fused peer-memory halo stores + flag handshake), and stats.
+// No CPU compute fallback exists: every step of the path runs in the kernels
+// of aw_kernels.cu / aw_stream.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/aw.h"
+#include "aw_internal.h"
+
+using aw::Coefs;
+using aw::Geom;
+using aw::Halo;
+
+namespace {
+
+thread_local std::string g_err;
+
+aw_status fail(aw_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+// ---------------------------------------------------------------------------
+// Exact FD weights: c_j = 2(-1)^{j+1}(m!)^2 / (j^2 (m-j)! (m+j)!),
+// c_0 = -2 sum c_j, as reduced rationals in 128-bit integers, then one
+// correctly rounded fp64 division each.
+// ---------------------------------------------------------------------------
+typedef __int128 i128;
+i128 igcd(i128 a, i128 b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        i128 t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+struct Rat {
+    i128 n, d;
+};
+Rat rat_norm(i128 n, i128 d) {
+    if (d < 0) n = -n, d = -d;
+    i128 g = igcd(n, d);
+    if (g == 0) g = 1;
+    return {n / g, d / g};
+}
+void fd_weights(int k, double* c) {
+    const int m = k / 2;
+    auto fact = [](int n) {
+        i128 f = 1;
+        for (int i = 2; i <= n; ++i) f *= i;
+        return f;
+    };
+    Rat sum{0, 1};
+    for (int j = 1; j <= m; ++j) {
+        i128 num = 2 * fact(m) * fact(m) * ((j % 2) ? 1 : -1);
+        i128 den = (i128)j * j * fact(m - j) * fact(m + j);
+        Rat cj = rat_norm(num, den);
+        c[j] = (double)(int64_t)cj.n / (double)(int64_t)cj.d;
+        sum = rat_norm(sum.n * cj.d + cj.n * sum.d, sum.d * cj.d);
+    }
+    Rat c0 = rat_norm(-2 * sum.n, sum.d);
+    c[0] = (double)(int64_t)c0.n / (double)(int64_t)c0.d;
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+enum PtrKind { PK_HOST, PK_DEVICE };
+PtrKind ptr_kind(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return PK_HOST;
+    }
+    return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? PK_DEVICE : PK_HOST;
+}
+
+struct Team;
+
+}  // namespace
+
+struct aw_grid {
+    // geometry
+    int ndim = 0;
+    int64_t shape[3] = {1, 1, 1};
+    double extent[3] = {0, 0, 0}, origin[3] = {0, 0, 0}, h[3] = {1, 1, 1};
+    int so = 0, R = 0;
+    int rank = 0, world = 1, device = 0;
+    int64_t z0 = 0;
+    Geom geom{};
+    Coefs coefs{};
+    // streams
+    cudaStream_t s = nullptr;
+    cudaStream_t ext = nullptr;
+    cudaEvent_t ev_sync = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    bool poisoned = false;
+    // device memory
+    float* ubuf[2] = {nullptr, nullptr};
+    size_t ubytes = 0;  // per wavefield buffer
+    float *m = nullptr, *eta = nullptr, *b = nullptr, *a = nullptr;
+    size_t mbytes = 0;
+    int64_t* d_base = nullptr;
+    unsigned* d_flag = nullptr;
+    unsigned long long* d_team_flags = nullptr;  // [2]: from rank-1, from rank+1
+    // state
+    bool have_model = false, have_damp = false, coeffs_valid = false, dt_set = false;
+    double dt = 0.0;
+    int cur = 0;  // physical buffer holding u^n
+    int64_t steps = 0;
+    // sources
+    int ns = 0, src_nt = 0;
+    std::vector<int64_t> src_corner_lin;  // [ns][nc]
+    std::vector<double> src_w64;          // [ns][nc]
+    std::vector<int> ent_src, ent_beta;   // owned entries in CSR order
+    float* d_wavelet = nullptr;
+    int64_t* d_inj_off = nullptr;
+    int* d_inj_plane = nullptr;
+    int* d_inj_ptr = nullptr;
+    int* d_inj_src = nullptr;
+    int64_t* d_inj_moff = nullptr;
+    double* d_inj_w64 = nullptr;
+    float* d_inj_s = nullptr;
+    int nuc = 0, nent = 0;
+    // receivers
+    int nr = 0, rec_nt = 0;
+    std::vector<int64_t> rec_corner_lin;
+    std::vector<float> rec_w32;
+    int nrl = 0;
+    int* d_rec_id = nullptr;
+    int64_t* d_rec_off = nullptr;
+    float* d_rec_w = nullptr;
+    float* d_traces = nullptr;
+    // options
+    int opt_kernel = AW_KERNEL_AUTO;
+    int opt_timing = 0;
+    int opt_graph = 16;
+    int opt_check = 1;
+    // stream kernel plan
+    aw::StreamPlan* plan = nullptr;
+    int eta_tiles_pct = 100;
+    int kernel_used = AW_KERNEL_V1;
+    // graphs: key = (G << 1) | parity
+    std::map<int64_t, cudaGraphExec_t> graphs;
+    // timing events pool
+    std::vector<cudaEvent_t> tev;
+    // team
+    Halo halo{};
+    unsigned long long* peer_flag_lo = nullptr;  // &flags_{rank-1}[1]
+    unsigned long long* peer_flag_hi = nullptr;  // &flags_{rank+1}[0]
+    std::vector<void*> ipc_opened;
+    bool team_connected = false;
+    bool halo_dirty = false;  // LOCAL set_wavefield in a team: exchange before the next run
+    int64_t nz_lo = 0;
+    unsigned long long epoch = 1;
+    // stats
+    aw_run_stats stats{};
+    int64_t launch_count = 0;  // kernels launched since creation
+};
+
+namespace {
+
+#define CK(call)                                                                                          \
+    do {                                                                                                  \
+        cudaError_t e_ = (call);                                                                          \
+        if (e_ != cudaSuccess) {                                                                          \
+            g->poisoned = true;                                                                           \
+            return fail(AW_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                                 \
+    } while (0)
+
+#define CHECK_STATE(g)                                                                 \
+    do {                                                                               \
+        if (!(g)) return fail(AW_EINVAL, "null grid handle");                          \
+        if ((g)->poisoned) return fail(AW_ESTATE, "handle poisoned by an earlier CUDA error"); \
+    } while (0)
+
+void free_graphs(aw_grid* g) {
+    for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+    g->graphs.clear();
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+// Synchronise the library stream with the caller's stream (entry) ...
+aw_status enter(aw_grid* g) {
+    cudaError_t e = cudaSetDevice(g->device);
+    if (e != cudaSuccess) {
+        g->poisoned = true;
+        return fail(AW_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    }
+    if (g->ext) {
+        CK(cudaEventRecord(g->ev_sync, g->ext));
+        CK(cudaStreamWaitEvent(g->s, g->ev_sync, 0));
+    }
+    return AW_OK;
+}
+// ... and back (exit): the caller's stream waits for the library's work.
+aw_status leave(aw_grid* g) {
+    if (g->ext) {
+        CK(cudaEventRecord(g->ev_sync, g->s));
+        CK(cudaStreamWaitEvent(g->ext, g->ev_sync, 0));
+    }
+    return AW_OK;
+}
+
+// Copy a dense [rows][nx] fp32 array (host or device) into a pitched device array.
+aw_status copy_in(aw_grid* g, float* dst, int64_t dst_pitch, const float* src, int64_t nx, int64_t rows) {
+    if (rows <= 0) return AW_OK;
+    cudaMemcpyKind kind = ptr_kind(src) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpy2DAsync(dst, dst_pitch * sizeof(float), src, nx * sizeof(float), nx * sizeof(float), rows, kind,
+                         g->s));
+    return AW_OK;
+}
+aw_status copy_out(aw_grid* g, float* dst, const float* src, int64_t src_pitch, int64_t nx, int64_t rows) {
+    if (rows <= 0) return AW_OK;
+    cudaMemcpyKind kind = ptr_kind(dst) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpy2DAsync(dst, nx * sizeof(float), src, src_pitch * sizeof(float), nx * sizeof(float), rows, kind,
+                         g->s));
+    return AW_OK;
+}
+
+int64_t rows_per_plane(const aw_grid* g) { return g->ndim == 3 ? g->shape[1] : 1; }
+int64_t nx_of(const aw_grid* g) { return g->shape[g->ndim - 1]; }
+
+// Sparse setup for one point: corners (global linear index,
+// -1 = skipped) and fp64 weights.  Returns false if the point is outside.
+bool locate(const aw_grid* g, const double* x, int64_t* corner, double* w, int64_t* base0) {
+    int64_t i[3];
+    double f[3];
+    for (int d = 0; d < g->ndim; ++d) {
+        double p = (x[d] - g->origin[d]) / g->h[d];
+        if (!(p >= 0.0 && p <= (double)(g->shape[d] - 1))) return false;
+        double fl = std::floor(p);
+        i[d] = (int64_t)fl;
+        f[d] = p - fl;
+    }
+    *base0 = i[0];
+    const int nc = 1 << g->ndim;
+    for (int beta = 0; beta < nc; ++beta) {
+        int64_t lin = 0;
+        double wt = 1.0;
+        bool skip = false;
+        for (int d = 0; d < g->ndim; ++d) {
+            const int up = (beta >> d) & 1;
+            const int64_t idx = i[d] + up;
+            if (idx >= g->shape[d]) skip = true;
+            const double wd = up ? f[d] : (1.0 - f[d]);
+            wt = (d == 0) ? wd : wt * wd;
+            lin = lin * g->shape[d] + idx;
+        }
+        corner[beta] = skip ? -1 : lin;
+        w[beta] = skip ? 0.0 : wt;
+    }
+    return true;
+}
+
+int64_t lin_div(const aw_grid* g) { return g->ndim == 3 ? g->shape[1] * g->shape[2] : g->shape[1]; }
+
+// global linear index -> (plane relative to z0, offset in a wavefield buffer, model index)
+void lin_to_local(const aw_grid* g, int64_t lin, int64_t* zl, int64_t* uoff, int64_t* moff) {
+    const int64_t per_plane = lin_div(g);
+    int64_t z = lin / per_plane;
+    int64_t rem = lin % per_plane;
+    int64_t y = 0, x = rem;
+    if (g->ndim == 3) {
+        y = rem / g->shape[2];
+        x = rem % g->shape[2];
+    }
+    *zl = z - g->z0;
+    *moff = (*zl) * g->geom.plane + y * g->geom.pitch + x;
+    *uoff = *moff + (int64_t)g->R * g->geom.plane;
+}
+
+unsigned long long enc(const aw_grid* g, int64_t level) {
+    return (g->epoch << 32) + (unsigned long long)(level + 1);
+}
+bool team_mode(const aw_grid* g) { return g->world > 1; }
+
+void free_sources(aw_grid* g) {
+    dfree(g->d_wavelet);
+    dfree(g->d_inj_off);
+    dfree(g->d_inj_plane);
+    dfree(g->d_inj_ptr);
+    dfree(g->d_inj_src);
+    dfree(g->d_inj_moff);
+    dfree(g->d_inj_w64);
+    dfree(g->d_inj_s);
+    g->ns = g->src_nt = g->nuc = g->nent = 0;
+    g->src_corner_lin.clear();
+    g->src_w64.clear();
+    g->ent_src.clear();
+    g->ent_beta.clear();
+}
+void free_receivers(aw_grid* g) {
+    dfree(g->d_rec_id);
+    dfree(g->d_rec_off);
+    dfree(g->d_rec_w);
+    dfree(g->d_traces);
+    g->nr = g->rec_nt = g->nrl = 0;
+    g->rec_corner_lin.clear();
+    g->rec_w32.clear();
+}
+
+template <class T>
+aw_status upload(aw_grid* g, T** dst, const std::vector<T>& v) {
+    dfree(*dst);
+    if (v.empty()) return AW_OK;
+    CK(cudaMalloc((void**)dst, v.size() * sizeof(T)));
+    CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g->s));
+    return AW_OK;
+}
+
+aw::Sparse sparse_view(const aw_grid* g) {
+    aw::Sparse sp{};
+    sp.nrl = g->nrl;
+    sp.nr = g->nr;
+    sp.rec_id = g->d_rec_id;
+    sp.rec_off = g->d_rec_off;
+    sp.rec_w = g->d_rec_w;
+    sp.traces = g->d_traces;
+    sp.nuc = g->nuc;
+    sp.ns = g->ns;
+    sp.inj_off = g->d_inj_off;
+    sp.inj_plane = g->d_inj_plane;
+    sp.inj_ptr = g->d_inj_ptr;
+    sp.inj_src = g->d_inj_src;
+    sp.inj_s = g->d_inj_s;
+    sp.wavelet = g->d_wavelet;
+    sp.nc = 1 << g->ndim;
+    return sp;
+}
+
+// dt-dependent tables: b, a, source scales, the streaming plan.
+aw_status prepare(aw_grid* g, double dt) {
+    if (g->coeffs_valid && g->dt_set && g->dt == dt) return AW_OK;
+    int64_t n = (int64_t)g->geom.nz * g->geom.plane;
+    CK(aw::launch_coeffs(g->m, g->have_damp ? g->eta : nullptr, g->b, g->have_damp ? g->a : nullptr, n, dt, g->s));
+    CK(aw::launch_source_scales(g->m, g->have_damp ? g->eta : nullptr, g->d_inj_moff, g->d_inj_w64, g->d_inj_s,
+                                g->nent, dt, g->s));
+    g->launch_count += 1 + (g->nent > 0 ? 1 : 0);
+    if (g->plan) {
+        aw::stream_release(g->plan);
+        g->plan = nullptr;
+    }
+    g->kernel_used = AW_KERNEL_V1;
+    g->eta_tiles_pct = g->have_damp ? 100 : 0;
+    if (g->opt_kernel != AW_KERNEL_V1 && g->ndim == 3) {
+        const float* ub[2] = {g->ubuf[0], g->ubuf[1]};
+        cudaError_t e = aw::stream_prepare(g->geom, ub, g->have_damp ? g->a : nullptr, &g->plan, &g->eta_tiles_pct,
+                                           g->s);
+        if (e == cudaSuccess) {
+            g->kernel_used = AW_KERNEL_STREAM;
+            g->launch_count += 1;
+        } else if (e == cudaErrorNotSupported) {
+            cudaGetLastError();
+            if (g->opt_kernel == AW_KERNEL_STREAM)
+                return fail(AW_EUNSUPPORTED, "no streaming-kernel specialisation for this configuration");
+        } else {
+            CK(e);
+        }
+    } else if (g->opt_kernel == AW_KERNEL_STREAM) {
+        return fail(AW_EUNSUPPORTED, "the streaming kernel is 3D only");
+    }
+    free_graphs(g);
+    g->dt = dt;
+    g->dt_set = true;
+    g->coeffs_valid = true;
+    return AW_OK;
+}
+
+// Enqueue one time step (local index i relative to *d_base) reading buffer
+// `cur` (u^n) and writing buffer 1-cur (u^{n+1} over u^{n-1}).
+aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0, cudaEvent_t e1, int64_t* launches) {
+    const int nxt = 1 - cur;
+    if (team_mode(g)) {
+        unsigned long long want_lo = g->halo.lo[0] ? enc(g, level) : 0ull;
+        unsigned long long want_hi = g->halo.hi[0] ? enc(g, level) : 0ull;
+        CK(aw::launch_team_wait(g->d_team_flags, want_lo, want_hi, g->s));
+        ++*launches;
+    }
+    if (e0) CK(cudaEventRecord(e0, g->s));
+    if (g->kernel_used == AW_KERNEL_STREAM) {
+        CK(aw::launch_stencil_stream(g->plan, g->geom, g->coefs, cur, g->ubuf[cur], g->ubuf[nxt], g->b,
+                                     g->have_damp ? g->a : nullptr, g->halo, nxt, g->s));
+    } else {
+        CK(aw::launch_stencil_v1(g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->b, g->have_damp ? g->a : nullptr,
+                                 g->halo, nxt, g->s));
+    }
+    ++*launches;
+    if (e1) CK(cudaEventRecord(e1, g->s));
+    if (g->nrl + g->nuc > 0) {
+        CK(aw::launch_sparse_step(g->geom, sparse_view(g), g->ubuf[cur], g->ubuf[nxt], g->d_base, i, g->halo, nxt,
+                                  g->s));
+        ++*launches;
+    }
+    if (team_mode(g) && (g->peer_flag_lo || g->peer_flag_hi)) {
+        CK(aw::launch_team_signal(g->peer_flag_lo, g->peer_flag_hi, g->epoch << 32, g->d_base, i, g->s));
+        ++*launches;
+    }
+    return AW_OK;
+}
+
+aw_status get_graph(aw_grid* g, int G, int cur, cudaGraphExec_t* out) {
+    int64_t key = ((int64_t)G << 1) | cur;
+    auto it = g->graphs.find(key);
+    if (it != g->graphs.end()) {
+        *out = it->second;
+        return AW_OK;
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(g->s, cudaStreamCaptureModeThreadLocal));
+    int64_t dummy = 0;
+    int c = cur;
+    aw_status st = AW_OK;
+    for (int i = 0; i < G && st == AW_OK; ++i) {
+        st = enqueue_step(g, i, c, 0, nullptr, nullptr, &dummy);
+        c = 1 - c;
+    }
+    if (st == AW_OK) {
+        cudaError_t e = aw::launch_advance(g->d_base, G, g->s);
+        if (e != cudaSuccess) st = fail(AW_ECUDA, "advance: %s", cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaStreamEndCapture(g->s, &graph);
+    if (st != AW_OK) {
+        g->poisoned = true;
+        return st;
+    }
+    CK(e);
+    cudaGraphExec_t exec;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    g->graphs[key] = exec;
+    *out = exec;
+    return AW_OK;
+}
+
+aw_status check_run_args(aw_grid* g, int nt, double dt) {
+    if (nt < 0) return fail(AW_EINVAL, "nt must be >= 0 (got %d)", nt);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(AW_EINVAL, "dt must be finite and > 0");
+    if (!g->have_model) return fail(AW_ESTATE, "aw_set_model has not been called");
+    if (g->dt_set && g->steps > 0 && dt != g->dt)
+        return fail(AW_EINVAL, "dt is fixed at %.17g until aw_reset (got %.17g)", g->dt, dt);
+    if (g->ns > 0 && g->steps + nt > g->src_nt)
+        return fail(AW_EINVAL, "wavelet covers %d steps, run needs %lld", g->src_nt, (long long)(g->steps + nt));
+    if (g->nr > 0 && g->steps + nt > g->rec_nt)
+        return fail(AW_EINVAL, "trace buffer covers %d steps, run needs %lld", g->rec_nt,
+                    (long long)(g->steps + nt));
+    return AW_OK;
+}
+
+// Copy my boundary planes of the current level into the neighbours' halos
+// (after a LOCAL set_wavefield) and publish the level.
+aw_status team_prologue(aw_grid* g) {
+    const int64_t R = g->R, plane = g->geom.plane;
+    const int c = g->cur;
+    if (g->halo.lo[c]) {
+        CK(cudaMemcpyAsync(g->halo.lo[c] + g->halo.lo_off, g->ubuf[c] + R * plane, R * plane * sizeof(float),
+                           cudaMemcpyDefault, g->s));
+    }
+    if (g->halo.hi[c]) {
+        CK(cudaMemcpyAsync(g->halo.hi[c] + g->halo.hi_off, g->ubuf[c] + (int64_t)g->geom.nz * plane,
+                           R * plane * sizeof(float), cudaMemcpyDefault, g->s));
+    }
+    CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, g->steps), g->s));
+    return AW_OK;
+}
+
+aw_status run_begin(aw_grid* g, int nt, double dt) {
+    aw_status st = check_run_args(g, nt, dt);
+    if (st) return st;
+    if (team_mode(g) && !g->team_connected) return fail(AW_ESTATE, "team handle is not connected");
+    if ((st = enter(g))) return st;
+    if ((st = prepare(g, dt))) return st;
+    if (g->halo_dirty) {
+        if ((st = team_prologue(g))) return st;
+        g->halo_dirty = false;
+    }
+    CK(cudaEventRecord(g->ev_t0, g->s));
+    int64_t base = g->steps;
+    CK(cudaMemcpyAsync(g->d_base, &base, sizeof base, cudaMemcpyHostToDevice, g->s));
+    CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
+    return AW_OK;
+}
+
+// Enqueue the nt steps.  Direct launches (with per-stencil events when
+// timing) or graphs of G steps.
+aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
+    const bool timing = g->opt_timing != 0;
+    const int G = g->opt_graph;
+    if (timing && (int64_t)g->tev.size() < 2 * (int64_t)nt) {
+        while ((int64_t)g->tev.size() < 2 * (int64_t)nt) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            g->tev.push_back(e);
+        }
+    }
+    int done = 0;
+    if (!timing && !team_mode(g) && G > 0) {
+        while (nt - done >= G) {
+            cudaGraphExec_t exec;
+            aw_status st = get_graph(g, G, g->cur, &exec);
+            if (st) return st;
+            CK(cudaGraphLaunch(exec, g->s));
+            *launches += (int64_t)G * (1 + (g->nrl + g->nuc > 0 ? 1 : 0)) + 1;
+            done += G;
+            if (G & 1) g->cur = 1 - g->cur;
+        }
+        // the graphs advanced *d_base to steps + done
+    }
+    const int first = done;
+    for (int i = 0; done < nt; ++i, ++done) {
+        cudaEvent_t e0 = timing ? g->tev[2 * i] : nullptr, e1 = timing ? g->tev[2 * i + 1] : nullptr;
+        aw_status st = enqueue_step(g, done - first, g->cur, g->steps + done, e0, e1, launches);
+        if (st) return st;
+        g->cur = 1 - g->cur;
+    }
+    return AW_OK;
+}
+
+aw_status run_end(aw_grid* g, int nt, int64_t launches) {
+    const int64_t t0 = g->steps;
+    if (g->opt_check) {
+        CK(aw::launch_check_finite(g->geom, g->ubuf[g->cur], g->nr > 0 ? g->d_traces : nullptr, t0, t0 + nt,
+                                   g->nr, g->d_flag, g->s));
+        ++launches;
+    }
+    CK(cudaEventRecord(g->ev_t1, g->s));
+    aw_status st = leave(g);
+    if (st) return st;
+    CK(cudaStreamSynchronize(g->s));
+    unsigned flag = 0;
+    CK(cudaMemcpy(&flag, g->d_flag, sizeof flag, cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, g->ev_t0, g->ev_t1));
+    g->stats.ms_total = ms;
+    g->stats.launches = launches;
+    g->launch_count += launches;
+    g->stats.launches_total = g->launch_count;
+    g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
+    g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
+    g->stats.kernel = g->kernel_used;
+    g->stats.eta_tiles = g->eta_tiles_pct;
+    if (g->opt_timing) {
+        double sum = 0.0;
+        for (int i = 0; i < nt; ++i) {
+            float e = 0.f;
+            CK(cudaEventElapsedTime(&e, g->tev[2 * i], g->tev[2 * i + 1]));
+            sum += e;
+        }
+        g->stats.ms_stencil = sum;
+        g->stats.n_stencil = nt;
+    } else {
+        g->stats.ms_stencil = -1.0;
+        g->stats.n_stencil = 0;
+    }
+    g->steps += nt;
+    if (flag) return fail(AW_ENONFINITE, "NaN/Inf in the wavefield or traces after steps [%lld, %lld)",
+                          (long long)t0, (long long)g->steps);
+    return AW_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* aw_last_error(void) { return g_err.c_str(); }
+int aw_abi_version(void) { return AW_ABI_VERSION; }
+
+double aw_critical_dt(int ndim, const double* spacing, int space_order, double vmax) {
+    if (ndim < 1 || ndim > 3 || !spacing || space_order < 2 || space_order > 16 || (space_order & 1) || !(vmax > 0))
+        return 0.0;
+    double c[AW_MAXR + 1];
+    fd_weights(space_order, c);
+    double S = std::fabs(c[0]);
+    for (int j = 1; j <= space_order / 2; ++j) S += 2.0 * std::fabs(c[j]);
+    double sum = 0.0;
+    for (int d = 0; d < ndim; ++d) sum += S / (spacing[d] * spacing[d]);
+    return 2.0 / (vmax * std::sqrt(sum));
+}
+
+aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const double* extent, const double* origin,
+                         int space_order, const aw_dist* dist) {
+    if (!out) return fail(AW_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (ndim == 1) return fail(AW_EUNSUPPORTED, "1D grids are not supported");
+    if (ndim < 2 || ndim > 3) return fail(AW_EINVAL, "ndim must be 2 or 3 (got %d)", ndim);
+    if (!shape || !extent) return fail(AW_EINVAL, "shape/extent is NULL");
+    if (space_order < 2 || space_order > 16 || (space_order & 1))
+        return fail(AW_EINVAL, "space_order must be even in [2, 16] (got %d)", space_order);
+    const int R = space_order / 2;
+    for (int d = 0; d < ndim; ++d) {
+        if (shape[d] < R + 1) return fail(AW_EINVAL, "shape[%d]=%lld < k/2+1", d, (long long)shape[d]);
+        if (shape[d] > (1ll << 31) - 1) return fail(AW_EINVAL, "shape[%d] too large", d);
+        if (!(extent[d] > 0.0) || !std::isfinite(extent[d])) return fail(AW_EINVAL, "extent[%d] must be > 0", d);
+        if (origin && !std::isfinite(origin[d])) return fail(AW_EINVAL, "origin[%d] not finite", d);
+    }
+    int rank = 0, world = 1, device = -1;
+    cudaStream_t ext = nullptr;
+    if (dist) {
+        rank = dist->rank;
+        world = dist->world;
+        device = dist->device;
+        ext = (cudaStream_t)dist->stream;
+        if (world < 1 || rank < 0 || rank >= world) return fail(AW_EINVAL, "bad rank/world %d/%d", rank, world);
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(AW_ECUDA, "no CUDA device available (libaw has no CPU fallback)");
+    }
+    if (device < 0) {
+        if (cudaGetDevice(&device) != cudaSuccess) return fail(AW_ECUDA, "cudaGetDevice failed");
+    }
+    if (device >= ndev) return fail(AW_EINVAL, "device %d >= device count %d", device, ndev);
+    // slab of axis 0: nearly equal split
+    const int64_t n0 = shape[0];
+    const int64_t base = n0 / world, rem = n0 % world;
+    const int64_t nz = base + (rank < rem ? 1 : 0);
+    const int64_t z0 = rank * base + std::min<int64_t>(rank, rem);
+    if (world > 1 && nz < R) return fail(AW_EINVAL, "slab of %lld planes is thinner than k/2=%d", (long long)nz, R);
+
+    aw_grid* g = new aw_grid();
+    g->ndim = ndim;
+    g->so = space_order;
+    g->R = R;
+    g->rank = rank;
+    g->world = world;
+    g->device = device;
+    g->z0 = z0;
+    g->ext = ext;
+    for (int d = 0; d < ndim; ++d) {
+        g->shape[d] = shape[d];
+        g->extent[d] = extent[d];
+        g->origin[d] = origin ? origin[d] : 0.0;
+        g->h[d] = extent[d] / (double)(shape[d] - 1);
+    }
+    Geom& G = g->geom;
+    G.ndim = ndim;
+    G.R = R;
+    G.nz = (int)nz;
+    G.ny = (int)rows_per_plane(g);
+    G.nx = (int)nx_of(g);
+    G.pitch = round_up(G.nx, AW_PITCH_ALIGN);
+    G.plane = (int64_t)G.ny * G.pitch;
+    // axis coefficients
+    double c[AW_MAXR + 1];
+    fd_weights(space_order, c);
+    double s0 = 0.0;
+    std::memset(&g->coefs, 0, sizeof g->coefs);
+    for (int d = 0; d < ndim; ++d) {
+        double h2 = g->h[d] * g->h[d];
+        for (int j = 1; j <= R; ++j) g->coefs.C[d][j] = (float)(c[j] / h2);
+        g->coefs.C[d][0] = (float)(c[0] / h2);
+        s0 = s0 + c[0] / h2;
+    }
+    g->coefs.C0 = (float)s0;
+
+    aw_status st = AW_OK;
+    auto bad = [&](cudaError_t e, const char* what) {
+        if (e == cudaSuccess) return false;
+        st = fail(e == cudaErrorMemoryAllocation ? AW_ENOMEM : AW_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+        cudaGetLastError();
+        return true;
+    };
+    do {
+        if (bad(cudaSetDevice(device), "cudaSetDevice")) break;
+        if (bad(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking), "stream")) break;
+        if (bad(cudaEventCreateWithFlags(&g->ev_sync, cudaEventDisableTiming), "event")) break;
+        if (bad(cudaEventCreate(&g->ev_t0), "event") || bad(cudaEventCreate(&g->ev_t1), "event")) break;
+        g->ubytes = (size_t)(nz + 2 * R) * G.plane * sizeof(float);
+        g->mbytes = (size_t)nz * G.plane * sizeof(float);
+        if (bad(cudaMalloc((void**)&g->ubuf[0], g->ubytes), "cudaMalloc u0")) break;
+        if (bad(cudaMalloc((void**)&g->ubuf[1], g->ubytes), "cudaMalloc u1")) break;
+        if (bad(cudaMalloc((void**)&g->m, g->mbytes), "cudaMalloc m")) break;
+        if (bad(cudaMalloc((void**)&g->b, g->mbytes), "cudaMalloc b")) break;
+        if (bad(cudaMalloc((void**)&g->d_base, sizeof(int64_t)), "cudaMalloc base")) break;
+        if (bad(cudaMalloc((void**)&g->d_flag, sizeof(unsigned)), "cudaMalloc flag")) break;
+        if (bad(cudaMalloc((void**)&g->d_team_flags, 2 * sizeof(unsigned long long)), "cudaMalloc flags")) break;
+        if (bad(cudaMemsetAsync(g->ubuf[0], 0, g->ubytes, g->s), "memset")) break;
+        if (bad(cudaMemsetAsync(g->ubuf[1], 0, g->ubytes, g->s), "memset")) break;
+        if (bad(cudaMemsetAsync(g->d_team_flags, 0, 2 * sizeof(unsigned long long), g->s), "memset")) break;
+        if (bad(cudaStreamSynchronize(g->s), "sync")) break;
+    } while (0);
+    if (st != AW_OK) {
+        aw_grid_destroy(g);
+        return st;
+    }
+    *out = g;
+    return AW_OK;
+}
+
+void aw_grid_destroy(aw_grid* g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    if (g->s) cudaStreamSynchronize(g->s);
+    free_graphs(g);
+    if (g->plan) aw::stream_release(g->plan);
+    for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
+    free_sources(g);
+    free_receivers(g);
+    dfree(g->ubuf[0]);
+    dfree(g->ubuf[1]);
+    dfree(g->m);
+    dfree(g->eta);
+    dfree(g->b);
+    dfree(g->a);
+    dfree(g->d_base);
+    dfree(g->d_flag);
+    dfree(g->d_team_flags);
+    for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
+    if (g->ev_sync) cudaEventDestroy(g->ev_sync);
+    if (g->ev_t0) cudaEventDestroy(g->ev_t0);
+    if (g->ev_t1) cudaEventDestroy(g->ev_t1);
+    if (g->s) cudaStreamDestroy(g->s);
+    cudaGetLastError();
+    delete g;
+}
+
+aw_status aw_local_extent(const aw_grid* g, int64_t* z0, int64_t* nz) {
+    if (!g) return fail(AW_EINVAL, "null grid handle");
+    if (z0) *z0 = g->z0;
+    if (nz) *nz = g->geom.nz;
+    return AW_OK;
+}
+
+int64_t aw_steps_done(const aw_grid* g) { return g ? g->steps : -1; }
+
+aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout) {
+    CHECK_STATE(g);
+    if (!m) return fail(AW_EINVAL, "m is NULL");
+    if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
+    aw_status st = enter(g);
+    if (st) return st;
+    const int64_t nx = g->geom.nx, rows = (int64_t)g->geom.nz * g->geom.ny;
+    const int64_t src_off = layout == AW_GLOBAL ? g->z0 * g->geom.ny * nx : 0;
+    if (damp && !g->eta) {
+        CK(cudaMalloc((void**)&g->eta, g->mbytes));
+        CK(cudaMalloc((void**)&g->a, g->mbytes));
+    }
+    // padding columns: m = 1, eta = 0 (never read as domain points)
+    CK(cudaMemsetAsync(g->m, 0, g->mbytes, g->s));
+    if ((st = copy_in(g, g->m, g->geom.pitch, m + src_off, nx, rows))) return st;
+    if (damp) {
+        CK(cudaMemsetAsync(g->eta, 0, g->mbytes, g->s));
+        if ((st = copy_in(g, g->eta, g->geom.pitch, damp + src_off, nx, rows))) return st;
+    }
+    CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
+    CK(aw::launch_validate_model(g->m, damp ? g->eta : nullptr, g->geom, g->d_flag, g->s));
+    g->launch_count += 1;
+    unsigned flag = 0;
+    CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof flag, cudaMemcpyDeviceToHost, g->s));
+    CK(cudaStreamSynchronize(g->s));
+    if ((st = leave(g))) return st;
+    if (flag) {
+        g->have_model = false;
+        g->coeffs_valid = false;
+        return fail(AW_EINVAL, "model invalid: m must be finite and > 0, damp finite and >= 0");
+    }
+    g->have_model = true;
+    g->have_damp = damp != nullptr;
+    g->coeffs_valid = false;
+    return AW_OK;
+}
+
+aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, const float* wavelet) {
+    CHECK_STATE(g);
+    if (ns < 0) return fail(AW_EINVAL, "ns < 0");
+    if (ns > 0 && (!coords || !wavelet || nt_max <= 0)) return fail(AW_EINVAL, "coords/wavelet/nt_max invalid");
+    const int nc = 1 << g->ndim;
+    std::vector<int64_t> corner((size_t)ns * nc);
+    std::vector<double> w((size_t)ns * nc);
+    for (int s = 0; s < ns; ++s) {
+        int64_t b0;
+        if (!locate(g, coords + (size_t)s * g->ndim, &corner[(size_t)s * nc], &w[(size_t)s * nc], &b0))
+            return fail(AW_EINVAL, "source %d lies outside the grid", s);
+    }
+    aw_status st = enter(g);
+    if (st) return st;
+    free_sources(g);
+    g->coeffs_valid = false;
+    if (ns == 0) return leave(g);
+    g->ns = ns;
+    g->src_nt = nt_max;
+    g->src_corner_lin = corner;
+    g->src_w64 = w;
+    // owned entries in CSR order: corner ascending, then source ascending (Q11)
+    struct E {
+        int64_t lin;
+        int s, beta;
+    };
+    std::vector<E> ents;
+    for (int s = 0; s < ns; ++s)
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t lin = corner[(size_t)s * nc + beta];
+            if (lin < 0) continue;
+            int64_t z = lin / lin_div(g);
+            if (z < g->z0 || z >= g->z0 + g->geom.nz) continue;
+            ents.push_back({lin, s, beta});
+        }
+    std::stable_sort(ents.begin(), ents.end(), [](const E& a, const E& b) {
+        return a.lin != b.lin ? a.lin < b.lin : (a.s != b.s ? a.s < b.s : a.beta < b.beta);
+    });
+    std::vector<int64_t> inj_off, inj_moff;
+    std::vector<int> inj_plane, inj_ptr, inj_src;
+    std::vector<double> inj_w;
+    for (size_t e = 0; e < ents.size(); ++e) {
+        if (e == 0 || ents[e].lin != ents[e - 1].lin) {
+            int64_t zl, uoff, moff;
+            lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
+            inj_off.push_back(uoff);
+            inj_plane.push_back((int)zl);
+            inj_ptr.push_back((int)e);
+        }
+        int64_t zl, uoff, moff;
+        lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
+        inj_moff.push_back(moff);
+        inj_src.push_back(ents[e].s);
+        inj_w.push_back(w[(size_t)ents[e].s * nc + ents[e].beta]);
+        g->ent_src.push_back(ents[e].s);
+        g->ent_beta.push_back(ents[e].beta);
+    }
+    inj_ptr.push_back((int)ents.size());
+    g->nuc = (int)inj_off.size();
+    g->nent = (int)ents.size();
+    if ((st = upload(g, &g->d_inj_off, inj_off)) || (st = upload(g, &g->d_inj_plane, inj_plane)) ||
+        (st = upload(g, &g->d_inj_ptr, inj_ptr)) || (st = upload(g, &g->d_inj_src, inj_src)) ||
+        (st = upload(g, &g->d_inj_moff, inj_moff)) || (st = upload(g, &g->d_inj_w64, inj_w)))
+        return st;
+    if (g->nent > 0) CK(cudaMalloc((void**)&g->d_inj_s, g->nent * sizeof(float)));
+    CK(cudaMalloc((void**)&g->d_wavelet, (size_t)nt_max * ns * sizeof(float)));
+    cudaMemcpyKind kind = ptr_kind(wavelet) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(g->d_wavelet, wavelet, (size_t)nt_max * ns * sizeof(float), kind, g->s));
+    CK(cudaStreamSynchronize(g->s));
+    return leave(g);
+}
+
+aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max) {
+    CHECK_STATE(g);
+    if (nr < 0) return fail(AW_EINVAL, "nr < 0");
+    if (nr > 0 && (!coords || nt_max <= 0)) return fail(AW_EINVAL, "coords/nt_max invalid");
+    const int nc = 1 << g->ndim;
+    std::vector<int64_t> corner((size_t)nr * nc), base0(nr);
+    std::vector<double> w((size_t)nr * nc);
+    for (int r = 0; r < nr; ++r)
+        if (!locate(g, coords + (size_t)r * g->ndim, &corner[(size_t)r * nc], &w[(size_t)r * nc], &base0[r]))
+            return fail(AW_EINVAL, "receiver %d lies outside the grid", r);
+    aw_status st = enter(g);
+    if (st) return st;
+    free_receivers(g);
+    free_graphs(g);
+    if (nr == 0) return leave(g);
+    g->nr = nr;
+    g->rec_nt = nt_max;
+    g->rec_corner_lin = corner;
+    g->rec_w32.resize(w.size());
+    for (size_t i = 0; i < w.size(); ++i) g->rec_w32[i] = (float)w[i];
+    // owner = rank owning the base corner's plane; its +1 corner may be a halo plane
+    std::vector<int> ids;
+    std::vector<int64_t> offs;
+    std::vector<float> ws;
+    for (int r = 0; r < nr; ++r) {
+        if (base0[r] < g->z0 || base0[r] >= g->z0 + g->geom.nz) continue;
+        ids.push_back(r);
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t lin = corner[(size_t)r * nc + beta];
+            if (lin < 0) {
+                offs.push_back(-1);
+                ws.push_back(0.f);
+                continue;
+            }
+            int64_t zl, uoff, moff;
+            lin_to_local(g, lin, &zl, &uoff, &moff);
+            offs.push_back(uoff);
+            ws.push_back(g->rec_w32[(size_t)r * nc + beta]);
+        }
+    }
+    g->nrl = (int)ids.size();
+    if ((st = upload(g, &g->d_rec_id, ids)) || (st = upload(g, &g->d_rec_off, offs)) ||
+        (st = upload(g, &g->d_rec_w, ws)))
+        return st;
+    CK(cudaMalloc((void**)&g->d_traces, (size_t)nt_max * nr * sizeof(float)));
+    CK(cudaMemsetAsync(g->d_traces, 0, (size_t)nt_max * nr * sizeof(float), g->s));
+    CK(cudaStreamSynchronize(g->s));
+    return leave(g);
+}
+
+aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, int layout) {
+    CHECK_STATE(g);
+    if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
+    aw_status st = enter(g);
+    if (st) return st;
+    const int64_t nx = g->geom.nx, ny = g->geom.ny, plane = g->geom.plane, R = g->R, nz = g->geom.nz;
+    const int64_t per_plane = ny * nx;  // dense elements per plane
+    for (int which = 0; which < 2; ++which) {
+        float* buf = g->ubuf[which == 0 ? g->cur : 1 - g->cur];
+        const float* src = which == 0 ? u_cur : u_prev;
+        CK(cudaMemsetAsync(buf, 0, g->ubytes, g->s));
+        if (!src) continue;
+        int64_t zlo = 0, zhi = nz;  // local planes to fill
+        if (layout == AW_GLOBAL && which == 0 && team_mode(g)) {
+            zlo = std::max<int64_t>(-R, -g->z0);
+            zhi = std::min<int64_t>(nz + R, g->shape[0] - g->z0);
+        }
+        const float* s0 = layout == AW_GLOBAL ? src + (g->z0 + zlo) * per_plane : src + zlo * per_plane;
+        if ((st = copy_in(g, buf + (zlo + R) * plane, g->geom.pitch, s0, nx, (zhi - zlo) * ny))) return st;
+    }
+    if (team_mode(g)) {
+        // New epoch: stale signals can no longer satisfy a wait.  With a GLOBAL array my halos are
+        // already filled, so tell the neighbours they may proceed (their step stores into my
+        // buffers only after this).  LOCAL: the exchange happens at the next aw_run (prologue).
+        g->epoch += 1;
+        if (layout == AW_GLOBAL) {
+            CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, g->steps), g->s));
+            g->launch_count += 1;
+        }
+    }
+    CK(cudaStreamSynchronize(g->s));
+    g->halo_dirty = team_mode(g) && layout == AW_LOCAL;
+    return leave(g);
+}
+
+aw_status aw_run(aw_grid* g, int nt, double dt) {
+    CHECK_STATE(g);
+    aw_status st = run_begin(g, nt, dt);
+    if (st) return st;
+    int64_t launches = 0;
+    if ((st = run_enqueue(g, nt, &launches))) return st;
+    return run_end(g, nt, launches);
+}
+
+aw_status aw_reset(aw_grid* g) {
+    CHECK_STATE(g);
+    aw_status st = enter(g);
+    if (st) return st;
+    CK(cudaMemsetAsync(g->ubuf[0], 0, g->ubytes, g->s));
+    CK(cudaMemsetAsync(g->ubuf[1], 0, g->ubytes, g->s));
+    if (g->d_traces) CK(cudaMemsetAsync(g->d_traces, 0, (size_t)g->rec_nt * g->nr * sizeof(float), g->s));
+    g->steps = 0;
+    g->cur = 0;
+    g->dt_set = false;
+    g->coeffs_valid = false;
+    if (team_mode(g)) {
+        // after my memsets: neighbours may start storing level-1 halos into my buffers
+        g->epoch += 1;
+        CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, 0), g->s));
+        g->launch_count += 1;
+    }
+    CK(cudaStreamSynchronize(g->s));
+    return leave(g);
+}
+
+aw_status aw_read_wavefield(aw_grid* g, int which, float* out, int layout) {
+    CHECK_STATE(g);
+    if (!out) return fail(AW_EINVAL, "out is NULL");
+    if (which != 0 && which != 1) return fail(AW_EINVAL, "which must be 0 or 1");
+    if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
+    aw_status st = enter(g);
+    if (st) return st;
+    const float* buf = g->ubuf[which == 0 ? g->cur : 1 - g->cur];
+    const int64_t nx = g->geom.nx, ny = g->geom.ny;
+    float* dst = layout == AW_GLOBAL ? out + g->z0 * ny * nx : out;
+    if ((st = copy_out(g, dst, buf + (int64_t)g->R * g->geom.plane, g->geom.pitch, nx, (int64_t)g->geom.nz * ny)))
+        return st;
+    CK(cudaStreamSynchronize(g->s));
+    return leave(g);
+}
+
+aw_status aw_read_receivers(aw_grid* g, float* out) {
+    CHECK_STATE(g);
+    if (g->nr == 0 || g->steps == 0) return AW_OK;
+    if (!out) return fail(AW_EINVAL, "out is NULL");
+    aw_status st = enter(g);
+    if (st) return st;
+    size_t bytes = (size_t)g->steps * g->nr * sizeof(float);
+    cudaMemcpyKind kind = ptr_kind(out) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpyAsync(out, g->d_traces, bytes, kind, g->s));
+    CK(cudaStreamSynchronize(g->s));
+    return leave(g);
+}
+
+aw_status aw_debug_sparse(const aw_grid* gc, int which, int64_t* corner_lin, float* w) {
+    aw_grid* g = const_cast<aw_grid*>(gc);
+    CHECK_STATE(g);
+    const int nc = 1 << g->ndim;
+    if (which == 1) {
+        if (corner_lin) std::copy(g->rec_corner_lin.begin(), g->rec_corner_lin.end(), corner_lin);
+        if (w) std::copy(g->rec_w32.begin(), g->rec_w32.end(), w);
+        return AW_OK;
+    }
+    if (which != 0) return fail(AW_EINVAL, "which must be 0 or 1");
+    if (corner_lin) std::copy(g->src_corner_lin.begin(), g->src_corner_lin.end(), corner_lin);
+    if (w) {
+        std::fill(w, w + (size_t)g->ns * nc, 0.0f);
+        if (g->nent > 0) {
+            std::vector<float> s(g->nent);
+            CK(cudaSetDevice(g->device));
+            CK(cudaMemcpy(s.data(), g->d_inj_s, g->nent * sizeof(float), cudaMemcpyDeviceToHost));
+            for (int e = 0; e < g->nent; ++e) w[(size_t)g->ent_src[e] * nc + g->ent_beta[e]] = s[e];
+        }
+    }
+    return AW_OK;
+}
+
+aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out) {
+    if (!g || !out) return fail(AW_EINVAL, "null argument");
+    *out = g->stats;
+    out->launches_total = g->launch_count;
+    return AW_OK;
+}
+
+aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
+    CHECK_STATE(g);
+    switch (option) {
+        case AW_OPT_KERNEL:
+            if (value < AW_KERNEL_AUTO || value > AW_KERNEL_STREAM) return fail(AW_EINVAL, "bad kernel %lld", (long long)value);
+            g->opt_kernel = (int)value;
+            g->coeffs_valid = false;
+            return AW_OK;
+        case AW_OPT_TIMING:
+            g->opt_timing = value != 0;
+            return AW_OK;
+        case AW_OPT_GRAPH_STEPS:
+            if (value < 0 || value > 4096) return fail(AW_EINVAL, "graph steps out of range");
+            g->opt_graph = (int)value;
+            free_graphs(g);
+            return AW_OK;
+        case AW_OPT_CHECK_FINITE:
+            g->opt_check = value != 0;
+            return AW_OK;
+        default:
+            return fail(AW_EINVAL, "unknown option %d", option);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Teams
+// ---------------------------------------------------------------------------
+struct aw_team_record {
+    cudaIpcMemHandle_t u[2];
+    cudaIpcMemHandle_t flags;
+    int64_t nz, R, plane, ny, nx;
+    int32_t rank, world;
+};
+
+size_t aw_team_export_size(void) { return sizeof(aw_team_record); }
+
+aw_status aw_team_export(aw_grid* g, void* out) {
+    CHECK_STATE(g);
+    if (!out) return fail(AW_EINVAL, "out is NULL");
+    aw_team_record rec;
+    std::memset(&rec, 0, sizeof rec);
+    CK(cudaSetDevice(g->device));
+    CK(cudaIpcGetMemHandle(&rec.u[0], g->ubuf[0]));
+    CK(cudaIpcGetMemHandle(&rec.u[1], g->ubuf[1]));
+    CK(cudaIpcGetMemHandle(&rec.flags, g->d_team_flags));
+    rec.nz = g->geom.nz;
+    rec.R = g->R;
+    rec.plane = g->geom.plane;
+    rec.ny = g->geom.ny;
+    rec.nx = g->geom.nx;
+    rec.rank = g->rank;
+    rec.world = g->world;
+    std::memcpy(out, &rec, sizeof rec);
+    return AW_OK;
+}
+
+static aw_status link_neighbours(aw_grid* g, float* lo0, float* lo1, unsigned long long* lo_flags, int64_t nz_lo,
+                                 float* hi0, float* hi1, unsigned long long* hi_flags) {
+    g->halo.lo[0] = lo0;
+    g->halo.lo[1] = lo1;
+    g->halo.hi[0] = hi0;
+    g->halo.hi[1] = hi1;
+    g->nz_lo = nz_lo;
+    g->halo.lo_off = lo0 ? (nz_lo + g->R) * g->geom.plane : 0;
+    g->halo.hi_off = 0;
+    g->peer_flag_lo = lo_flags ? lo_flags + 1 : nullptr;  // I am rank+1 of my lower neighbour
+    g->peer_flag_hi = hi_flags ? hi_flags + 0 : nullptr;  // I am rank-1 of my upper neighbour
+    g->team_connected = true;
+    free_graphs(g);
+    return AW_OK;
+}
+
+aw_status aw_team_connect(aw_grid* g, const void* all_records) {
+    CHECK_STATE(g);
+    if (!all_records) return fail(AW_EINVAL, "records NULL");
+    if (!team_mode(g)) {
+        g->team_connected = true;
+        return AW_OK;
+    }
+    const aw_team_record* recs = (const aw_team_record*)all_records;
+    for (int r = 0; r < g->world; ++r)
+        if (recs[r].rank != r || recs[r].world != g->world || recs[r].plane != g->geom.plane || recs[r].R != g->R)
+            return fail(AW_EINVAL, "inconsistent team record of rank %d", r);
+    CK(cudaSetDevice(g->device));
+    void* p[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+    void* f[2] = {nullptr, nullptr};
+    const int nb[2] = {g->rank - 1, g->rank + 1};
+    for (int k = 0; k < 2; ++k) {
+        int r = nb[k];
+        if (r < 0 || r >= g->world) continue;
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaIpcOpenMemHandle(&p[k][b], recs[r].u[b], cudaIpcMemLazyEnablePeerAccess));
+            g->ipc_opened.push_back(p[k][b]);
+        }
+        CK(cudaIpcOpenMemHandle(&f[k], recs[r].flags, cudaIpcMemLazyEnablePeerAccess));
+        g->ipc_opened.push_back(f[k]);
+    }
+    int64_t nz_lo = g->rank > 0 ? recs[g->rank - 1].nz : 0;
+    link_neighbours(g, (float*)p[0][0], (float*)p[0][1], (unsigned long long*)f[0], nz_lo, (float*)p[1][0],
+                    (float*)p[1][1], (unsigned long long*)f[1]);
+    CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, g->steps), g->s));
+    CK(cudaStreamSynchronize(g->s));
+    return AW_OK;
+}
+
+aw_status aw_team_connect_local(aw_grid** grids, int world) {
+    if (!grids || world < 1) return fail(AW_EINVAL, "bad team");
+    for (int r = 0; r < world; ++r) {
+        if (!grids[r] || grids[r]->rank != r || grids[r]->world != world)
+            return fail(AW_EINVAL, "grid %d is not rank %d of a %d-slab team", r, r, world);
+        if (grids[r]->poisoned) return fail(AW_ESTATE, "grid %d poisoned", r);
+    }
+    for (int r = 0; r < world; ++r) {
+        aw_grid* g = grids[r];
+        aw_grid* lo = r > 0 ? grids[r - 1] : nullptr;
+        aw_grid* hi = r + 1 < world ? grids[r + 1] : nullptr;
+        if (lo && lo->device != g->device) {
+            cudaSetDevice(g->device);
+            cudaDeviceEnablePeerAccess(lo->device, 0);
+            cudaGetLastError();
+        }
+        if (hi && hi->device != g->device) {
+            cudaSetDevice(g->device);
+            cudaDeviceEnablePeerAccess(hi->device, 0);
+            cudaGetLastError();
+        }
+        link_neighbours(g, lo ? lo->ubuf[0] : nullptr, lo ? lo->ubuf[1] : nullptr, lo ? lo->d_team_flags : nullptr,
+                        lo ? lo->geom.nz : 0, hi ? hi->ubuf[0] : nullptr, hi ? hi->ubuf[1] : nullptr,
+                        hi ? hi->d_team_flags : nullptr);
+    }
+    for (int r = 0; r < world; ++r) {
+        aw_grid* g = grids[r];
+        CK(cudaSetDevice(g->device));
+        CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, g->steps), g->s));
+        CK(cudaStreamSynchronize(g->s));
+    }
+    return AW_OK;
+}
+
+aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt) {
+    if (!grids || world < 1) return fail(AW_EINVAL, "bad team");
+    for (int r = 0; r < world; ++r) {
+        CHECK_STATE(grids[r]);
+        if (grids[r]->steps != grids[0]->steps) return fail(AW_ESTATE, "ranks are at different steps");
+    }
+    for (int r = 0; r < world; ++r) {
+        aw_status st = run_begin(grids[r], nt, dt);
+        if (st) return st;
+    }
+    std::vector<int64_t> launches(world, 0);
+    // interleave the ranks step by step on their own streams
+    for (int i = 0; i < nt; ++i) {
+        for (int r = 0; r < world; ++r) {
+            aw_grid* g = grids[r];
+            if (g->opt_timing && (int64_t)g->tev.size() < 2 * (int64_t)nt) {
+                while ((int64_t)g->tev.size() < 2 * (int64_t)nt) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreate(&e));
+                    g->tev.push_back(e);
+                }
+            }
+            cudaEvent_t e0 = g->opt_timing ? g->tev[2 * i] : nullptr, e1 = g->opt_timing ? g->tev[2 * i + 1] : nullptr;
+            CK(cudaSetDevice(g->device));
+            aw_status st = enqueue_step(g, i, g->cur, g->steps + i, e0, e1, &launches[r]);
+            if (st) return st;
+            g->cur = 1 - g->cur;
+        }
+    }
+    aw_status result = AW_OK;
+    for (int r = 0; r < world; ++r) {
+        aw_grid* g = grids[r];
+        CK(cudaSetDevice(g->device));
+        aw_status st = run_end(g, nt, launches[r]);
+        if (st && result == AW_OK) result = st;
+    }
+    return result;
+}
+
+}  // extern "C"
+

@@ -1,0 +1,93 @@
+// aw_internal.h -- private declarations of libaw (host runtime <-> device kernels).
+// Not part of the ABI; see include/aw.h for the public boundary.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define AW_MAXR 8          // space order <= 16
+#define AW_PITCH_ALIGN 32  // x pitch in floats (128 B rows: coalescing + TMA 16-B strides)
+
+namespace aw {
+
+// Axis coefficients of the star Laplacian, fp32:
+// C[d][j] = fl32(c_j / h_d^2), C0 = fl32(sum_d c_0 / h_d^2).
+struct Coefs {
+    float C[3][AW_MAXR + 1];
+    float C0;
+};
+
+// Geometry of one rank's device arrays.  Wavefield buffers hold planes
+// [-R, nz+R) of axis 0 (halo planes: zero at the global ends, the neighbour's
+// boundary planes inside a team); model/coefficient arrays hold [0, nz).
+// 2D grids use ny = 1 (axes (z, x)).
+struct Geom {
+    int ndim;
+    int R;
+    int nz, ny, nx;      // owned planes, axis-1 points (1 in 2D), x points
+    int64_t pitch;       // floats per x row
+    int64_t plane;       // ny * pitch
+};
+
+// Peer targets for the fused halo stores (team mode); null when absent.
+struct Halo {
+    float* lo[2];   // rank-1's buffers (base = its plane -R); my planes [0,R) go to its planes [nz_lo, nz_lo+R)
+    float* hi[2];   // rank+1's buffers; my planes [nz-R, nz) go to its planes [-R, 0)
+    int64_t lo_off; // element offset of rank-1's plane nz_lo relative to its base
+    int64_t hi_off; // element offset of rank+1's plane -R relative to its base (= 0)
+};
+
+// Sparse (receivers + injection CSR) device view
+struct Sparse {
+    // receivers owned by this rank
+    int nrl;                 // number of owned receivers
+    int nr;                  // global receiver count (trace row length)
+    const int* rec_id;       // [nrl] global receiver index
+    const int64_t* rec_off;  // [nrl][nc] element offset into a wavefield buffer (-1 = skipped)
+    const float* rec_w;      // [nrl][nc]
+    float* traces;           // [nt_max][nr]
+    // injection CSR by corner (ascending global linear index)
+    int nuc;                 // unique owned corners
+    int ns;                  // global source count (wavelet row length)
+    const int64_t* inj_off;  // [nuc] element offset into a wavefield buffer
+    const int* inj_plane;    // [nuc] local plane index (for halo propagation)
+    const int* inj_ptr;      // [nuc+1]
+    const int* inj_src;      // [nent]
+    const float* inj_s;      // [nent] fp32 scales
+    const float* wavelet;    // [nt_max][ns]
+    int nc;                  // 2^ndim
+};
+
+// ---- kernels / launchers (aw_kernels.cu) ----
+cudaError_t launch_coeffs(const float* m, const float* eta, float* b, float* a, int64_t n, double dt,
+                          cudaStream_t s);
+cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag,
+                                  cudaStream_t s);
+cudaError_t launch_source_scales(const float* m, const float* eta, const int64_t* moff, const double* w64,
+                                 float* s_out, int nent, double dt, cudaStream_t s);
+cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, float* unext,
+                              const float* b, const float* a, const Halo& halo, int parity_next,
+                              cudaStream_t s);
+cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucur, float* unext,
+                               const int64_t* d_base, int i, const Halo& halo, int parity_next,
+                               cudaStream_t s);
+cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s);
+cudaError_t launch_check_finite(const Geom& g, const float* u, const float* traces, int64_t t0,
+                                int64_t t1, int nr, unsigned* flag, cudaStream_t s);
+cudaError_t launch_team_wait(const volatile unsigned long long* flags, unsigned long long want_lo,
+                             unsigned long long want_hi, cudaStream_t s);
+cudaError_t launch_team_signal(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
+                               unsigned long long add, const int64_t* d_base, int i, cudaStream_t s);
+cudaError_t launch_team_raise(unsigned long long* f0, unsigned long long* f1, unsigned long long v,
+                              cudaStream_t s);
+
+// 2.5D z-streaming kernel (aw_stream.cu); returns cudaErrorNotSupported when
+// the configuration has no streaming specialisation.
+struct StreamPlan;
+cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* a, StreamPlan** plan,
+                           int* eta_tiles_pct, cudaStream_t s);
+void stream_release(StreamPlan* p);
+cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
+                                  const float* ucur, float* unext, const float* b, const float* a,
+                                  const Halo& halo, int parity_next, cudaStream_t s);
+
+}  // namespace aw

@@ -1,0 +1,304 @@
+// aw_kernels.cu -- reference-grade device kernels of libaw (sm_100a).
+//
+// Every floating-point operation of the update is written with an explicit
+// rounding intrinsic (__fmul_rn/__fadd_rn/__fsub_rn/__fmaf_rn) so that nvcc can
+// neither contract nor reorder it: the per-point sequence is the canonical one
+// of SURVEY.md §8(c).6 (restated in DESIGN.md §2), which makes the GPU
+// value-identical to the fp32 oracle rather than merely close.
+//
+//   L   = C0 * u_p                                        (PAPER.md:417 centre term)
+//   for d = ndim-1 .. 0, j = 1..R:  L = fma(C[d][j], u_{p-j e_d} + u_{p+j e_d}, L)
+//   t   = 2 u_p - u^{n-1}_p
+//   w   = fma(b_p, L, t)                                  (b = dt^2/m, division hoisted,
+//   u^{n+1}_p = fma(a_p, w, (1 - a_p) * u^{n-1}_p)         PAPER.md:788-826; a = m/(m+eta dt/2))
+#include "aw_internal.h"
+
+namespace aw {
+
+// ---------------------------------------------------------------------------
+// Coefficient precompute, fp64 then one rounding to fp32.
+// ---------------------------------------------------------------------------
+__global__ void coeffs_kernel(const float* __restrict__ m, const float* __restrict__ eta,
+                              float* __restrict__ b, float* __restrict__ a, int64_t n, double dt) {
+    const double dt2 = __dmul_rn(dt, dt);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double mm = (double)m[i];
+        double e = eta ? (double)eta[i] : 0.0;
+        double den = __dadd_rn(mm, __dmul_rn(__dmul_rn(e, dt), 0.5));
+        b[i] = __double2float_rn(__ddiv_rn(dt2, mm));
+        if (a) a[i] = __double2float_rn(__ddiv_rn(mm, den));
+    }
+}
+
+cudaError_t launch_coeffs(const float* m, const float* eta, float* b, float* a, int64_t n, double dt,
+                          cudaStream_t s) {
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    coeffs_kernel<<<blocks, 256, 0, s>>>(m, eta, b, a, n, dt);
+    return cudaGetLastError();
+}
+
+// Model validation: m > 0 finite, eta >= 0 finite at every owned point.
+__global__ void validate_kernel(const float* __restrict__ m, const float* __restrict__ eta, int nz, int ny,
+                                int nx, int64_t pitch, unsigned* flag) {
+    int64_t rows = (int64_t)nz * ny;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* mr = m + r * pitch;
+        const float* er = eta ? eta + r * pitch : nullptr;
+        for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+            float v = mr[x];
+            bool bad = !(v > 0.0f) || !isfinite(v);
+            if (er) {
+                float e = er[x];
+                bad |= !(e >= 0.0f) || !isfinite(e);
+            }
+            if (bad) atomicOr(flag, 1u);
+        }
+    }
+}
+
+cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag,
+                                  cudaStream_t s) {
+    int64_t rows = (int64_t)g.nz * g.ny;
+    int blocks = (int)(rows < 148 * 8 ? rows : 148 * 8);
+    if (blocks < 1) blocks = 1;
+    validate_kernel<<<blocks, 128, 0, s>>>(m, eta, g.nz, g.ny, g.nx, g.pitch, flag);
+    return cudaGetLastError();
+}
+
+// Source scales s = fl32((w64 * dt^2) / (m_c + (eta_c * dt) * 0.5))
+__global__ void source_scales_kernel(const float* __restrict__ m, const float* __restrict__ eta,
+                                     const int64_t* __restrict__ moff, const double* __restrict__ w64,
+                                     float* __restrict__ s_out, int nent, double dt) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nent) return;
+    int64_t o = moff[i];
+    double mm = (double)m[o];
+    double e = eta ? (double)eta[o] : 0.0;
+    double den = __dadd_rn(mm, __dmul_rn(__dmul_rn(e, dt), 0.5));
+    double dt2 = __dmul_rn(dt, dt);
+    s_out[i] = __double2float_rn(__ddiv_rn(__dmul_rn(w64[i], dt2), den));
+}
+
+cudaError_t launch_source_scales(const float* m, const float* eta, const int64_t* moff, const double* w64,
+                                 float* s_out, int nent, double dt, cudaStream_t s) {
+    if (nent <= 0) return cudaSuccess;
+    source_scales_kernel<<<(nent + 127) / 128, 128, 0, s>>>(m, eta, moff, w64, s_out, nent, dt);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// v1 stencil: one thread per point, global loads, canonical op order.
+// Zero ghosts: x/y by bounds checks, z by the (zeroed or exchanged) halo planes.
+// In a team the first/last R owned planes are also stored into the
+// neighbours' halo planes (peer memory) -- the fused exchange.
+// ---------------------------------------------------------------------------
+template <int NDIM, int R>
+__global__ void __launch_bounds__(256) stencil_v1_kernel(Geom g, Coefs c, const float* __restrict__ ucur,
+                                                         float* __restrict__ unext, const float* __restrict__ b,
+                                                         const float* __restrict__ a, float* __restrict__ lo,
+                                                         int64_t lo_off, float* __restrict__ hi, int64_t hi_off) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = (NDIM == 3) ? (int)(blockIdx.y * blockDim.y + threadIdx.y) : 0;
+    const int z = (NDIM == 3) ? (int)blockIdx.z : (int)(blockIdx.y * blockDim.y + threadIdx.y);
+    if (x >= g.nx || y >= g.ny || z >= g.nz) return;
+    const int64_t o = (int64_t)z * g.plane + (int64_t)y * g.pitch + x;  // model index
+    const int64_t ou = o + (int64_t)R * g.plane;                          // wavefield index
+    const float* p = ucur + ou;
+    const float uc = p[0];
+    float L = __fmul_rn(c.C0, uc);
+    // axis ndim-1 (x, contiguous)
+#pragma unroll
+    for (int j = 1; j <= R; ++j) {
+        float lo_v = (x - j >= 0) ? p[-j] : 0.0f;
+        float hi_v = (x + j < g.nx) ? p[j] : 0.0f;
+        L = __fmaf_rn(c.C[NDIM - 1][j], __fadd_rn(lo_v, hi_v), L);
+    }
+    if (NDIM == 3) {
+        // axis 1 (y)
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            float lo_v = (y - j >= 0) ? p[-(int64_t)j * g.pitch] : 0.0f;
+            float hi_v = (y + j < g.ny) ? p[(int64_t)j * g.pitch] : 0.0f;
+            L = __fmaf_rn(c.C[1][j], __fadd_rn(lo_v, hi_v), L);
+        }
+    }
+    // axis 0 (z): halo planes
+#pragma unroll
+    for (int j = 1; j <= R; ++j)
+        L = __fmaf_rn(c.C[0][j], __fadd_rn(p[-(int64_t)j * g.plane], p[(int64_t)j * g.plane]), L);
+    const float um = unext[ou];  // u^{n-1} lives in the output buffer (in place)
+    const float t = __fsub_rn(__fmul_rn(2.0f, uc), um);
+    const float w = __fmaf_rn(b[o], L, t);
+    const float aa = a ? a[o] : 1.0f;
+    const float r = __fmul_rn(__fsub_rn(1.0f, aa), um);
+    const float un = __fmaf_rn(aa, w, r);
+    unext[ou] = un;
+    if (lo && z < R) lo[lo_off + o] = un;
+    if (hi && z >= g.nz - R) hi[hi_off + o - (int64_t)(g.nz - R) * g.plane] = un;
+}
+
+template <int NDIM>
+static cudaError_t launch_v1_ndim(const Geom& g, const Coefs& c, const float* ucur, float* unext, const float* b,
+                                  const float* a, float* lo, int64_t lo_off, float* hi, int64_t hi_off,
+                                  cudaStream_t s) {
+    dim3 block, grid;
+    if (NDIM == 3) {
+        block = dim3(64, 4, 1);
+        grid = dim3((g.nx + 63) / 64, (g.ny + 3) / 4, g.nz);
+    } else {
+        block = dim3(128, 2, 1);
+        grid = dim3((g.nx + 127) / 128, (g.nz + 1) / 2, 1);
+    }
+    switch (g.R) {
+#define AW_CASE(RR) \
+    case RR: stencil_v1_kernel<NDIM, RR><<<grid, block, 0, s>>>(g, c, ucur, unext, b, a, lo, lo_off, hi, hi_off); break;
+        AW_CASE(1) AW_CASE(2) AW_CASE(3) AW_CASE(4) AW_CASE(5) AW_CASE(6) AW_CASE(7) AW_CASE(8)
+#undef AW_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, float* unext, const float* b,
+                              const float* a, const Halo& halo, int parity_next, cudaStream_t s) {
+    float* lo = halo.lo[parity_next];
+    float* hi = halo.hi[parity_next];
+    if (g.ndim == 3) return launch_v1_ndim<3>(g, c, ucur, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
+    return launch_v1_ndim<2>(g, c, ucur, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
+}
+
+// ---------------------------------------------------------------------------
+// Per-step sparse work: receivers read u^n, injection adds into
+// u^{n+1} in CSR order (corner ascending, then source ascending; Q11).
+// Step index n = *d_base + i (d_base advanced once per graph / run chunk).
+// ---------------------------------------------------------------------------
+__global__ void sparse_step_kernel(Geom g, Sparse sp, const float* __restrict__ ucur, float* __restrict__ unext,
+                                   const int64_t* __restrict__ d_base, int i, float* __restrict__ lo,
+                                   int64_t lo_off, float* __restrict__ hi, int64_t hi_off) {
+    const int64_t n = *d_base + i;
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < sp.nrl) {
+        float acc = 0.0f;
+        for (int beta = 0; beta < sp.nc; ++beta) {
+            int64_t off = sp.rec_off[(int64_t)t * sp.nc + beta];
+            if (off < 0) continue;
+            acc = __fmaf_rn(sp.rec_w[(int64_t)t * sp.nc + beta], ucur[off], acc);
+        }
+        sp.traces[n * sp.nr + sp.rec_id[t]] = acc;
+        return;
+    }
+    t -= sp.nrl;
+    if (t < sp.nuc) {
+        const int64_t off = sp.inj_off[t];
+        float v = unext[off];
+        const float* q = sp.wavelet + n * sp.ns;
+        for (int e = sp.inj_ptr[t]; e < sp.inj_ptr[t + 1]; ++e) v = __fmaf_rn(sp.inj_s[e], q[sp.inj_src[e]], v);
+        unext[off] = v;
+        // keep the neighbours' halo copies of boundary planes consistent (team mode)
+        const int z = sp.inj_plane[t];
+        const int64_t o = off - (int64_t)g.R * g.plane;  // model-layout index
+        if (lo && z < g.R) lo[lo_off + o] = v;
+        if (hi && z >= g.nz - g.R) hi[hi_off + o - (int64_t)(g.nz - g.R) * g.plane] = v;
+    }
+}
+
+cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucur, float* unext,
+                               const int64_t* d_base, int i, const Halo& halo, int parity_next, cudaStream_t s) {
+    int n = sp.nrl + sp.nuc;
+    if (n <= 0) return cudaSuccess;
+    sparse_step_kernel<<<(n + 127) / 128, 128, 0, s>>>(g, sp, ucur, unext, d_base, i, halo.lo[parity_next],
+                                                       halo.lo_off, halo.hi[parity_next], halo.hi_off);
+    return cudaGetLastError();
+}
+
+__global__ void advance_kernel(int64_t* d_base, int64_t by) { *d_base += by; }
+
+cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s) {
+    advance_kernel<<<1, 1, 0, s>>>(d_base, by);
+    return cudaGetLastError();
+}
+
+// NaN/Inf check of the owned wavefield and of trace rows [t0, t1).
+__global__ void check_finite_kernel(Geom g, const float* __restrict__ u, const float* __restrict__ traces,
+                                    int64_t t0, int64_t t1, int nr, unsigned* flag) {
+    int64_t rows = (int64_t)g.nz * g.ny;
+    bool bad = false;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* ur = u + (int64_t)g.R * g.plane + r * g.pitch;
+        for (int x = threadIdx.x; x < g.nx; x += blockDim.x) bad |= !isfinite(ur[x]);
+    }
+    if (traces) {
+        int64_t tot = (t1 - t0) * nr;
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < tot; k += (int64_t)gridDim.x * blockDim.x)
+            bad |= !isfinite(traces[t0 * nr + k]);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+cudaError_t launch_check_finite(const Geom& g, const float* u, const float* traces, int64_t t0, int64_t t1,
+                                int nr, unsigned* flag, cudaStream_t s) {
+    check_finite_kernel<<<148 * 4, 256, 0, s>>>(g, u, traces, t0, t1, nr, flag);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Team handshake: after step n a rank publishes "level n+1 halo delivered"
+// into its neighbours' flag words (system-scope release); before step n a
+// rank waits until both neighbours published level n (acquire).  Because the
+// flag is raised only after the whole step (stencil + injection) completed,
+// it also certifies that the neighbour finished reading the halo buffer that
+// the next step overwrites (no WAR hazard with two physical levels).
+// ---------------------------------------------------------------------------
+__global__ void team_wait_kernel(const volatile unsigned long long* flags, unsigned long long want_lo,
+                                 unsigned long long want_hi) {
+    if (threadIdx.x != 0) return;
+    // flags[0]: from rank-1, flags[1]: from rank+1
+    for (;;) {
+        unsigned long long f0, f1;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f0) : "l"(flags + 0) : "memory");
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f1) : "l"(flags + 1) : "memory");
+        if (f0 >= want_lo && f1 >= want_hi) break;
+        __nanosleep(200);
+    }
+}
+
+cudaError_t launch_team_wait(const volatile unsigned long long* flags, unsigned long long want_lo,
+                             unsigned long long want_hi, cudaStream_t s) {
+    team_wait_kernel<<<1, 32, 0, s>>>(flags, want_lo, want_hi);
+    return cudaGetLastError();
+}
+
+__global__ void team_signal_kernel(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
+                                   unsigned long long add, const int64_t* d_base, int i) {
+    if (threadIdx.x != 0) return;
+    // enc(level) = (epoch << 32) + level + 1; this step produced level *d_base + i + 1
+    unsigned long long v = add + (unsigned long long)(*d_base + i + 2);
+    __threadfence_system();  // halo stores of this step (stencil + injection) before the flag
+    if (peer_lo_flag) atomicMax_system(peer_lo_flag, v);
+    if (peer_hi_flag) atomicMax_system(peer_hi_flag, v);
+}
+
+cudaError_t launch_team_signal(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
+                               unsigned long long add, const int64_t* d_base, int i, cudaStream_t s) {
+    team_signal_kernel<<<1, 32, 0, s>>>(peer_lo_flag, peer_hi_flag, add, d_base, i);
+    return cudaGetLastError();
+}
+
+// Raise flag words to at least v (monotone, so late signals of an older epoch never lower them).
+__global__ void team_raise_kernel(unsigned long long* f0, unsigned long long* f1, unsigned long long v) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    if (f0) atomicMax_system(f0, v);
+    if (f1) atomicMax_system(f1, v);
+}
+
+cudaError_t launch_team_raise(unsigned long long* f0, unsigned long long* f1, unsigned long long v,
+                              cudaStream_t s) {
+    team_raise_kernel<<<1, 32, 0, s>>>(f0, f1, v);
+    return cudaGetLastError();
+}
+
+}  // namespace aw
