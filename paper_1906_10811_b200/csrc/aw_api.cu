@@ -369,8 +369,8 @@ aw_status prepare(aw_grid* g, double dt) {
     g->eta_tiles_pct = g->have_damp ? 100 : 0;
     if (g->opt_kernel != AW_KERNEL_V1 && g->ndim == 3) {
         const float* ub[2] = {g->ubuf[0], g->ubuf[1]};
-        cudaError_t e = aw::stream_prepare(g->geom, ub, g->have_damp ? g->a : nullptr, &g->plan, &g->eta_tiles_pct,
-                                           g->s);
+        cudaError_t e = aw::stream_prepare(g->geom, ub, g->b, g->have_damp ? g->a : nullptr, &g->plan,
+                                           &g->eta_tiles_pct, g->s);
         if (e == cudaSuccess) {
             g->kernel_used = AW_KERNEL_STREAM;
             g->launch_count += 1;

@@ -83,8 +83,8 @@ cudaError_t launch_team_raise(unsigned long long* f0, unsigned long long* f1, un
 // 2.5D z-streaming kernel (aw_stream.cu); returns cudaErrorNotSupported when
 // the configuration has no streaming specialisation.
 struct StreamPlan;
-cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* a, StreamPlan** plan,
-                           int* eta_tiles_pct, cudaStream_t s);
+cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* b, const float* a,
+                           StreamPlan** plan, int* eta_tiles_pct, cudaStream_t s);
 void stream_release(StreamPlan* p);
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
                                   const float* ucur, float* unext, const float* b, const float* a,

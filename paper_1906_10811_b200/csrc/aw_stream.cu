@@ -1,17 +1,505 @@
-// aw_stream.cu -- 2.5D z-streaming stencil kernel (placeholder until the TMA kernel lands).
+// aw_stream.cu -- 2.5D z-streaming stencil kernel for 3D grids (sm_100a).
+//
+// The hot loop of the path (SURVEY.md §8(a) rows a5+a6): star Laplacian of
+// order k = 2R fused with the damped leapfrog update, HBM-bound (16 B per
+// point update).  Design (B200-first, not the paper's OPS code):
+//
+//  * persistent, load-balanced grid: exactly (#SMs x resident CTAs) CTAs; the
+//    flattened (xy-tile, z) index space is split into equal contiguous ranges,
+//    so every CTA streams the same number of planes (no wave tail);
+//  * each CTA streams its xy tile (TX x TY outputs) along z (axis 0).  One
+//    producer warp issues TMA (cp.async.bulk.tensor.3d) loads of the u^n
+//    plane tile with its halo, (TX+2R') x (TY+2R) floats, into a ring of
+//    SU = R+1+D shared-memory stages guarded by full/empty mbarriers.  TMA's
+//    out-of-bounds zero fill *is* the zero-ghost boundary in x and y
+//    (PAPER.md:455-491 zero padding); z ghosts are the zeroed halo planes;
+//  * consumer threads own RY consecutive y rows at one x: the z neighbours
+//    come from a per-thread register queue of 2R+1 centre values, the x and y
+//    neighbours from the resident stage of the output plane (y register
+//    blocking shares the column loads between the RY points);
+//  * u^{n-1}, b (and a, only in tiles/planes where eta != 0 -- a per
+//    (plane, tile) flag precomputed at prepare) are streamed with coalesced
+//    loads prefetched one plane ahead; u^{n+1} is stored in place over u^{n-1};
+//  * in a team, boundary planes are also stored straight into the
+//    neighbours' halo planes (peer memory over NVLink): the fused exchange.
+//
+// Per point the arithmetic is the canonical sequence of SURVEY §8(c).6 with
+// explicit-rounding intrinsics, so the result is value-identical to the fp32
+// oracle and to the v1 kernel:
+//   L = C0*u; x pairs j=1..R; y pairs; z pairs (fma each); t = 2u - u^{n-1};
+//   w = fma(b, L, t); u^{n+1} = fma(a, w, (1-a) u^{n-1}).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "aw_internal.h"
 
 namespace aw {
-struct StreamPlan {
-    int dummy;
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
+                 "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ float ldg_stream(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+template <int R_, int TX_, int TY_, int RY_, int D_, int PD_>
+struct Cfg {
+    static constexpr int R = R_, TX = TX_, TY = TY_, RY = RY_, D = D_, PD = PD_;
+    // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
+    // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
+    static constexpr int RP = (R + 3) / 4 * 4;
+    static constexpr int TXP = TX + 2 * RP;
+    static constexpr int TYP = TY + 2 * R;
+    static constexpr int SU = R + 1 + D;  // ring stages: planes [p-R, p+D]
+    static constexpr int NCOMP = TX * (TY / RY);
+    static constexpr int NWARPS_COMP = NCOMP / 32;
+    static constexpr int NTHREADS = NCOMP + 32;  // + one producer warp
+    static constexpr int STAGE_FLOATS = TXP * TYP;
+    static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;                 // TMA transaction bytes
+    static constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;  // 128-B aligned ring slots
+    static constexpr int STAGE_STRIDE_F = STAGE_STRIDE / 4;
+    static constexpr size_t SMEM = (size_t)SU * STAGE_STRIDE + 2 * SU * sizeof(uint64_t);
+    static_assert(TX % 32 == 0 && TY % RY == 0, "tile shape");
+    static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
 };
-cudaError_t stream_prepare(const Geom&, const float* const*, const float*, StreamPlan** plan, int*, cudaStream_t) {
+
+struct StreamArgs {
+    Geom g;
+    Coefs c;
+    float* unext;            // buffer base (plane -R)
+    const float* b;          // model layout
+    const float* a;          // may be null (no damping)
+    const uint8_t* flags;    // [nz][ntiles]: 1 if any a != 1 in the tile-plane
+    float* lo;               // team halo targets (null if none)
+    int64_t lo_off;
+    float* hi;
+    int64_t hi_off;
+    int ntx, nty;            // tiles along x, y
+    int64_t total;           // ntiles * nz work items
+    int64_t per;             // items per CTA
+};
+
+struct StreamMaps {
+    CUtensorMap u;    // u^n buffer, box (TXP, TYP, 1): loads into the ring (+ L2 prefetch)
+    CUtensorMap un;   // u^{n-1}/u^{n+1} buffer, box (TX, TY, 1): L2 prefetch of u^{n-1}
+    CUtensorMap b;    // model layout, box (TX, TY, 1)
+    CUtensorMap a;    // model layout, box (TX, TY, 1) (unused without damping)
+};
+
+}  // namespace
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, 1)
+    stream_kernel(const __grid_constant__ StreamMaps M, const __grid_constant__ StreamArgs A) {
+    constexpr int R = C::R, TX = C::TX, RY = C::RY, RP = C::RP, TXP = C::TXP, SU = C::SU, PD = C::PD;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)SU * C::STAGE_STRIDE);
+    uint64_t* empty = full + SU;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < SU; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NWARPS_COMP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const Geom& g = A.g;
+    const int nz = g.nz;
+    const int ntiles = A.ntx * A.nty;
+    const int64_t w_begin = (int64_t)blockIdx.x * A.per;
+    const int64_t w_end = min(A.total, w_begin + A.per);
+    if (w_begin >= w_end) return;
+
+    if (warp == C::NWARPS_COMP) {
+        // ---------------- producer warp ----------------
+        // TMA loads of u^n plane tiles (with halo) into the ring, D planes ahead of the
+        // consumers, and L2 prefetches PD planes ahead of everything the consumers stream
+        // (u^n tiles, and u^{n-1}, b, a tiles of the output planes).
+        if ((tid & 31) == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.u) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.un) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.b) : "memory");
+            if (A.a) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.a) : "memory");
+            uint32_t it = 0;
+            for (int64_t w = w_begin; w < w_end;) {
+                const int tile = (int)(w / nz);
+                const int zb = (int)(w % nz);
+                const int ze = (int)((int64_t)nz < zb + (w_end - w) ? (int64_t)nz : zb + (w_end - w));
+                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * C::TY;
+                const int niter = ze - zb + 2 * R;
+                auto l2_prefetch = [&](int kk) {
+                    // u^n plane zb-R+kk (buffer plane zb+kk) and the output plane zb-2R+kk's streams
+                    if (kk < niter) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + kk);
+                    const int zo = zb - 2 * R + kk;
+                    if (zo >= zb && zo < ze) {
+                        tma_prefetch_l2_3d(&M.un, x0, y0, zo + R);
+                        tma_prefetch_l2_3d(&M.b, x0, y0, zo);
+                        if (A.a && A.flags[(int64_t)zo * ntiles + tile]) tma_prefetch_l2_3d(&M.a, x0, y0, zo);
+                    }
+                };
+                for (int kk = 0; kk < PD; ++kk) l2_prefetch(kk);
+                for (int k = 0; k < niter; ++k, ++it) {
+                    l2_prefetch(k + PD);
+                    const int s = it % SU;
+                    const uint32_t ph = (it / SU) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], C::STAGE_BYTES);
+                    // plane p = zb - R + k lives at buffer plane p + R
+                    tma_load_3d(ring + (size_t)s * C::STAGE_STRIDE_F, &M.u, &full[s], x0 - RP, y0 - R, zb + k);
+                }
+                w += ze - zb;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    const int lx = tid % TX;
+    const int ly = (tid / TX) * RY;
+    const float C0 = A.c.C0;
+    uint32_t it = 0;
+    for (int64_t w = w_begin; w < w_end;) {
+        const int tile = (int)(w / nz);
+        const int zb = (int)(w % nz);
+        const int ze = (int)((int64_t)nz < zb + (w_end - w) ? (int64_t)nz : zb + (w_end - w));
+        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * C::TY;
+        const int x = x0 + lx;
+        const bool xin = x < g.nx;
+        const int niter = ze - zb + 2 * R;
+
+        float q[RY][2 * R + 1];
+#pragma unroll
+        for (int i = 0; i < RY; ++i)
+#pragma unroll
+            for (int j = 0; j <= 2 * R; ++j) q[i][j] = 0.0f;
+        // streams of the next output plane (L2 hits: the producer prefetched them)
+        float pu[RY], pb[RY], pa[RY];
+        auto fetch = [&](int z) {
+            const bool use_a = A.a != nullptr && A.flags[(int64_t)z * ntiles + tile];
+#pragma unroll
+            for (int i = 0; i < RY; ++i) {
+                const int y = y0 + ly + i;
+                const bool in = xin && y < g.ny;
+                const int64_t o = (int64_t)z * g.plane + (int64_t)y * g.pitch + x;
+                pu[i] = in ? ldg_stream(A.unext + o + (int64_t)R * g.plane) : 0.0f;
+                pb[i] = in ? ldg_stream(A.b + o) : 0.0f;
+                pa[i] = (in && use_a) ? ldg_stream(A.a + o) : 1.0f;
+            }
+        };
+        fetch(zb);
+
+        for (int k = 0; k < niter; ++k, ++it) {
+            const int s = it % SU;
+            const uint32_t ph = (it / SU) & 1;
+            mbar_wait(&full[s], ph);
+            const float* P = ring + (size_t)s * C::STAGE_STRIDE_F;
+            // shift the z queue and append the centre values of the newest plane
+#pragma unroll
+            for (int i = 0; i < RY; ++i) {
+#pragma unroll
+                for (int j = 0; j < 2 * R; ++j) q[i][j] = q[i][j + 1];
+                q[i][2 * R] = P[(ly + i + R) * TXP + lx + RP];
+            }
+            if (k >= 2 * R) {
+                const int z = zb + k - 2 * R;  // output plane; its stage is R iterations old
+                const float* Q = ring + (size_t)((it - R) % SU) * C::STAGE_STRIDE_F;
+                // column of the output plane: rows ly .. ly+RY-1+2R at this x
+                float col[RY + 2 * R];
+#pragma unroll
+                for (int r = 0; r < RY + 2 * R; ++r) col[r] = Q[(ly + r) * TXP + lx + RP];
+#pragma unroll
+                for (int i = 0; i < RY; ++i) {
+                    const float* row = Q + (ly + i + R) * TXP + lx + RP;
+                    const float uc = q[i][R];
+                    float L = __fmul_rn(C0, uc);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j) L = __fmaf_rn(A.c.C[2][j], __fadd_rn(row[-j], row[j]), L);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        L = __fmaf_rn(A.c.C[1][j], __fadd_rn(col[i + R - j], col[i + R + j]), L);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        L = __fmaf_rn(A.c.C[0][j], __fadd_rn(q[i][R - j], q[i][R + j]), L);
+                    const float t = __fsub_rn(__fmul_rn(2.0f, uc), pu[i]);
+                    const float wv = __fmaf_rn(pb[i], L, t);
+                    const float rr = __fmul_rn(__fsub_rn(1.0f, pa[i]), pu[i]);
+                    const float un = __fmaf_rn(pa[i], wv, rr);
+                    const int y = y0 + ly + i;
+                    if (xin && y < g.ny) {
+                        const int64_t o = (int64_t)z * g.plane + (int64_t)y * g.pitch + x;
+                        A.unext[o + (int64_t)R * g.plane] = un;
+                        if (A.lo && z < R) A.lo[A.lo_off + o] = un;
+                        if (A.hi && z >= nz - R) A.hi[A.hi_off + o - (int64_t)(nz - R) * g.plane] = un;
+                    }
+                }
+                if (z + 1 < ze) fetch(z + 1);
+            }
+            // release the stage of plane p - R (no longer needed by any later output)
+            if (k >= R) {
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive(&empty[(it - R) % SU]);
+            }
+        }
+        // release the last R stages of this segment (planes ze .. ze+R-1)
+#pragma unroll 1
+        for (int k = niter - R; k < niter; ++k) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[(it - (niter - k)) % SU]);
+        }
+        w += ze - zb;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// eta flags: flags[z][tile] = 1 iff some a != 1 in the tile-plane
+// ---------------------------------------------------------------------------
+__global__ void eta_flags_kernel(Geom g, const float* __restrict__ a, int TX, int TY, int ntx, int nty,
+                                 uint8_t* flags) {
+    const int tile = blockIdx.x;
+    const int z = blockIdx.y;
+    const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TY;
+    bool any = false;
+    for (int idx = threadIdx.x; idx < TX * TY; idx += blockDim.x) {
+        int x = x0 + idx % TX, y = y0 + idx / TX;
+        if (x < g.nx && y < g.ny) any |= a[(int64_t)z * g.plane + (int64_t)y * g.pitch + x] != 1.0f;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) flags[(int64_t)z * ntx * nty + tile] = any ? 1 : 0;
+}
+
+__global__ void count_flags_kernel(const uint8_t* flags, int64_t n, unsigned long long* cnt) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += flags[i];
+    atomicAdd(cnt, c);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct StreamPlan {
+    StreamMaps maps[2];  // by parity of the u^n buffer
+    uint8_t* flags = nullptr;
+    int ntx = 0, nty = 0;
+    int grid = 0;
+    int R = 0;
+    size_t smem = 0;
+    int nthreads = 0;
+    int TX = 0, TY = 0;
+};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+cudaError_t encode3d(CUtensorMap* m, const void* base, const Geom& g, int planes, int bx, int by) {
+    auto enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <class C>
+cudaError_t setup(StreamPlan* p, const Geom& g) {
+    p->smem = C::SMEM;
+    p->nthreads = C::NTHREADS;
+    p->TX = C::TX;
+    p->TY = C::TY;
+    cudaError_t e = cudaFuncSetAttribute(stream_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<C>, C::NTHREADS, C::SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorNotSupported;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    p->grid = sms * occ;
+    return cudaSuccess;
+}
+
+template <class C>
+cudaError_t make_maps(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a) {
+    for (int par = 0; par < 2; ++par) {
+        StreamMaps& M = p->maps[par];
+        cudaError_t e;
+        if ((e = encode3d(&M.u, ubuf[par], g, g.nz + 2 * g.R, C::TXP, C::TYP))) return e;
+        if ((e = encode3d(&M.un, ubuf[1 - par], g, g.nz + 2 * g.R, C::TX, C::TY))) return e;
+        if ((e = encode3d(&M.b, b, g, g.nz, C::TX, C::TY))) return e;
+        if ((e = encode3d(&M.a, a ? a : b, g, g.nz, C::TX, C::TY))) return e;
+    }
+    return cudaSuccess;
+}
+
+template <class C>
+cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, float* unext, const float* b,
+                   const float* a, const Halo& halo, int parity_next, cudaStream_t s) {
+    StreamArgs A;
+    A.g = g;
+    A.c = c;
+    A.unext = unext;
+    A.b = b;
+    A.a = a;
+    A.flags = p->flags;
+    A.lo = halo.lo[parity_next];
+    A.lo_off = halo.lo_off;
+    A.hi = halo.hi[parity_next];
+    A.hi_off = halo.hi_off;
+    A.ntx = p->ntx;
+    A.nty = p->nty;
+    A.total = (int64_t)p->ntx * p->nty * g.nz;
+    A.per = (A.total + p->grid - 1) / p->grid;
+    stream_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
+    return cudaGetLastError();
+}
+
+// configuration table: (R, TX, TY, RY, D = ring lookahead, PD = L2 prefetch distance)
+using C1 = Cfg<1, 64, 16, 4, 2, 6>;
+using C2 = Cfg<2, 64, 16, 4, 2, 6>;
+using C3 = Cfg<3, 64, 16, 4, 2, 6>;
+using C4 = Cfg<4, 64, 16, 4, 2, 6>;
+using C5 = Cfg<5, 64, 16, 4, 2, 6>;
+using C6 = Cfg<6, 64, 16, 4, 2, 6>;
+using C7 = Cfg<7, 64, 16, 4, 2, 6>;
+using C8 = Cfg<8, 64, 16, 4, 2, 6>;
+
+}  // namespace
+
+#define AW_STREAM_DISPATCH(R, EXPR)       \
+    switch (R) {                          \
+        case 1: { using C = C1; EXPR; } break; \
+        case 2: { using C = C2; EXPR; } break; \
+        case 3: { using C = C3; EXPR; } break; \
+        case 4: { using C = C4; EXPR; } break; \
+        case 5: { using C = C5; EXPR; } break; \
+        case 6: { using C = C6; EXPR; } break; \
+        case 7: { using C = C7; EXPR; } break; \
+        case 8: { using C = C8; EXPR; } break; \
+        default: return cudaErrorNotSupported; \
+    }
+
+cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* b, const float* a,
+                           StreamPlan** plan, int* eta_tiles_pct, cudaStream_t s) {
     *plan = nullptr;
+    if (g.ndim != 3) return cudaErrorNotSupported;
+    StreamPlan* p = new StreamPlan();
+    p->R = g.R;
+    cudaError_t e = cudaSuccess;
+    AW_STREAM_DISPATCH(g.R, e = setup<C>(p, g); if (e == cudaSuccess) e = make_maps<C>(p, g, ubuf, b, a));
+    if (e != cudaSuccess) {
+        delete p;
+        return e;
+    }
+    p->ntx = (g.nx + p->TX - 1) / p->TX;
+    p->nty = (g.ny + p->TY - 1) / p->TY;
+    const int64_t nflags = (int64_t)p->ntx * p->nty * g.nz;
+    e = cudaMalloc(&p->flags, nflags);
+    if (e != cudaSuccess) {
+        delete p;
+        return e;
+    }
+    if (a) {
+        dim3 grid(p->ntx * p->nty, g.nz);
+        eta_flags_kernel<<<grid, 256, 0, s>>>(g, a, p->TX, p->TY, p->ntx, p->nty, p->flags);
+        unsigned long long* cnt = nullptr;
+        e = cudaMallocAsync(&cnt, sizeof(unsigned long long), s);
+        if (e == cudaSuccess) {
+            cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s);
+            count_flags_kernel<<<148, 256, 0, s>>>(p->flags, nflags, cnt);
+            unsigned long long h = 0;
+            cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            cudaFreeAsync(cnt, s);
+            *eta_tiles_pct = (int)(100.0 * (double)h / (double)nflags + 0.5);
+        }
+    } else {
+        cudaMemsetAsync(p->flags, 0, nflags, s);
+        *eta_tiles_pct = 0;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFree(p->flags);
+        delete p;
+        return e;
+    }
+    *plan = p;
+    return cudaSuccess;
+}
+
+void stream_release(StreamPlan* p) {
+    if (!p) return;
+    if (p->flags) cudaFree(p->flags);
+    delete p;
+}
+
+cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur,
+                                  float* unext, const float* b, const float* a, const Halo& halo, int parity_next,
+                                  cudaStream_t s) {
+    (void)ucur;  // read through the tensor map of buffer parity_cur
+    if (!p) return cudaErrorNotSupported;
+    AW_STREAM_DISPATCH(p->R, return launch<C>(p, g, c, parity_cur, unext, b, a, halo, parity_next, s));
     return cudaErrorNotSupported;
 }
-void stream_release(StreamPlan* p) { delete p; }
-cudaError_t launch_stencil_stream(StreamPlan*, const Geom&, const Coefs&, int, const float*, float*, const float*,
-                                  const float*, const Halo&, int, cudaStream_t) {
-    return cudaErrorNotSupported;
-}
+
 }  // namespace aw
