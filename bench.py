@@ -281,24 +281,31 @@ def main():
         g.run(nt, spec["dt"])
         g.read_receivers(out=traces)
 
+    # per-launch CUDA events around the stencil kernel (the event pool is created in the warm-up)
+    g.set_option(aw.AW_OPT_TIMING, 1)
     for _ in range(args.warmup):
         one_step(m_dev, d_dev, wav_dev, traces_dev)
 
     # ---- timed region: K steps, inputs resident in HBM ----
-    g.set_option(aw.AW_OPT_TIMING, 1)  # per-launch CUDA events around the stencil kernel
     clocks = Clocks(local)
     launches0 = g.stats()["launches_total"]
     torch.cuda.synchronize()
     barrier()
-    clocks.start()
+    if not os.environ.get("AW_BENCH_NO_CLOCKS"):
+        clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    ms_stencil, n_stencil = 0.0, 0
+    ms_stencil, n_stencil, ms_runs = 0.0, 0, 0.0
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         one_step(m_dev, d_dev, wav_dev, traces_dev)
         st = g.stats()
         ms_stencil += st["ms_stencil"]
         n_stencil += st["n_stencil"]
+        ms_runs += st["ms_total"]
+        if os.environ.get("AW_BENCH_VERBOSE"):
+            print(f"step: wall {1e3 * (time.perf_counter() - t0):.2f} ms, run {st['ms_total']:.2f} ms, "
+                  f"stencil {st['ms_stencil']:.2f} ms", file=sys.stderr, flush=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()

@@ -1,36 +1,42 @@
 // aw_stream.cu -- 2.5D z-streaming stencil kernel for 3D grids (sm_100a).
 //
 // The hot loop of the path (SURVEY.md §8(a) rows a5+a6): star Laplacian of
-// order k = 2R fused with the damped leapfrog update, HBM-bound (16 B per
-// point update).  Design (B200-first, not the paper's OPS code):
+// order k = 2R fused with the damped leapfrog update.  It is HBM-bound at
+// 16 algorithmic B per point update, so the design goal is to
+// stream u^n, u^{n-1}, b (and a where eta != 0) exactly once from HBM and
+// write u^{n+1} once, with few enough instructions per point that the SMs
+// keep up with HBM.  B200-first choices (not the paper's OPS-generated code):
 //
-//  * persistent, load-balanced grid: exactly (#SMs x resident CTAs) CTAs; the
-//    flattened (xy-tile, z) index space is split into equal contiguous ranges,
-//    so every CTA streams the same number of planes (no wave tail);
-//  * each CTA streams its xy tile (TX x TY outputs) along z (axis 0).  One
-//    producer warp issues TMA (cp.async.bulk.tensor.3d) loads of the u^n
-//    plane tile with its halo, (TX+2R') x (TY+2R) floats, into a ring of
-//    SU = R+1+D shared-memory stages guarded by full/empty mbarriers.  TMA's
-//    out-of-bounds zero fill *is* the zero-ghost boundary in x and y
-//    (PAPER.md:455-491 zero padding); z ghosts are the zeroed halo planes;
-//  * consumer threads own RY consecutive y rows at one x: the z neighbours
-//    come from a per-thread register queue of 2R+1 centre values, the x and y
-//    neighbours from the resident stage of the output plane (y register
-//    blocking shares the column loads between the RY points);
-//  * u^{n-1}, b (and a, only in tiles/planes where eta != 0 -- a per
-//    (plane, tile) flag precomputed at prepare) are streamed with coalesced
-//    loads prefetched one plane ahead; u^{n+1} is stored in place over u^{n-1};
-//  * in a team, boundary planes are also stored straight into the
-//    neighbours' halo planes (peer memory over NVLink): the fused exchange.
+//  * persistent grid of (#SMs x resident CTAs) CTAs; work items are
+//    (xy tile, z chunk) pairs handed out cyclically, so at any time the
+//    resident CTAs work on neighbouring tiles at the same z and the halo rows
+//    one CTA loads are L2 hits for its neighbours;
+//  * one producer warp issues TMA (cp.async.bulk.tensor.3d) loads of the u^n
+//    plane tile with its halo into a ring of SU = R+1+D shared-memory stages
+//    (full/empty mbarriers), plus TMA L2 prefetches PD planes ahead for every
+//    stream the consumers read (u^n tiles, and the u^{n-1}, b, a tiles of
+//    the output planes).  TMA's out-of-bounds zero fill is the zero-ghost
+//    boundary in x and y; z ghosts are zeroed halo planes;
+//  * consumer warps: lane l owns the x columns x0+l and x0+l+32 of RY rows,
+//    so every operation is done on point pairs with the Blackwell packed-fp32
+//    instructions (FFMA2/FADD2/FMUL2, per-lane IEEE RN == the scalar ops);
+//  * z neighbours come from a register queue of 2R+1 centre values; the
+//    plane loop is unrolled by 2R+1 so the queue rotates by renaming, not by
+//    moves; x and y neighbours come from the resident stage of the output
+//    plane (the y column is loaded once per thread and shared by its rows);
+//  * interior tiles run a predicate-free path; edge tiles mask their loads
+//    and stores;
+//  * in a team, boundary planes are also stored into the neighbours' halo
+//    planes (peer memory over NVLink): the fused exchange.
 //
-// Per point the arithmetic is the canonical sequence of SURVEY §8(c).6 with
-// explicit-rounding intrinsics, so the result is value-identical to the fp32
-// oracle and to the v1 kernel:
+// Per point the arithmetic is the canonical sequence of SURVEY §8(c).6:
 //   L = C0*u; x pairs j=1..R; y pairs; z pairs (fma each); t = 2u - u^{n-1};
-//   w = fma(b, L, t); u^{n+1} = fma(a, w, (1-a) u^{n-1}).
+//   w = fma(b, L, t); u^{n+1} = fma(a, w, (1-a) u^{n-1})
+// so the result is value-identical to the fp32 oracle and the v1 kernel.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "aw_internal.h"
@@ -82,24 +88,37 @@ __device__ __forceinline__ float ldg_stream(const float* p) {
     return v;
 }
 
-template <int R_, int TX_, int TY_, int RY_, int D_, int PD_>
+// packed fp32 (Blackwell FFMA2/FADD2/FMUL2): per component identical to the scalar _rn ops
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
+template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_>
 struct Cfg {
-    static constexpr int R = R_, TX = TX_, TY = TY_, RY = RY_, D = D_, PD = PD_;
+    static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
+    static constexpr int Q = 2 * R + 1;  // z queue length (and plane-loop unroll)
     // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
     // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
     static constexpr int RP = (R + 3) / 4 * 4;
     static constexpr int TXP = TX + 2 * RP;
     static constexpr int TYP = TY + 2 * R;
-    static constexpr int SU = R + 1 + D;  // ring stages: planes [p-R, p+D]
-    static constexpr int NCOMP = TX * (TY / RY);
-    static constexpr int NWARPS_COMP = NCOMP / 32;
-    static constexpr int NTHREADS = NCOMP + 32;  // + one producer warp
+    static constexpr int SU = R + 1 + D;  // u^n ring: planes [p-R, p+D]
+    static constexpr int SP = DP + 1;     // (u^{n-1}, b, a) ring of the output planes
+    static constexpr int NWARPS_COMP = TY / RY;
+    static constexpr int NCOMP = 32 * NWARPS_COMP;
+    static constexpr int NTHREADS = NCOMP + 64;  // + producer warps for the u^n ring and the streams ring
     static constexpr int STAGE_FLOATS = TXP * TYP;
     static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;                 // TMA transaction bytes
     static constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;  // 128-B aligned ring slots
     static constexpr int STAGE_STRIDE_F = STAGE_STRIDE / 4;
-    static constexpr size_t SMEM = (size_t)SU * STAGE_STRIDE + 2 * SU * sizeof(uint64_t);
-    static_assert(TX % 32 == 0 && TY % RY == 0, "tile shape");
+    static constexpr int PTILE_FLOATS = TX * TY;
+    static constexpr int PTILE_BYTES = PTILE_FLOATS * 4;
+    static constexpr int PSTAGE_FLOATS = 3 * PTILE_FLOATS;  // u^{n-1}, b, a
+    static constexpr size_t U_BYTES = (size_t)SU * STAGE_STRIDE;
+    static constexpr size_t P_BYTES = (size_t)SP * PSTAGE_FLOATS * 4;
+    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t);
+    static_assert(TY % RY == 0, "tile shape");
     static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
 };
 
@@ -107,7 +126,6 @@ struct StreamArgs {
     Geom g;
     Coefs c;
     float* unext;            // buffer base (plane -R)
-    const float* b;          // model layout
     const float* a;          // may be null (no damping)
     const uint8_t* flags;    // [nz][ntiles]: 1 if any a != 1 in the tile-plane
     float* lo;               // team halo targets (null if none)
@@ -115,34 +133,172 @@ struct StreamArgs {
     float* hi;
     int64_t hi_off;
     int ntx, nty;            // tiles along x, y
-    int64_t total;           // ntiles * nz work items
-    int64_t per;             // items per CTA
+    int nzc, zc;             // z chunks and planes per chunk
+    int nitems;              // ntiles * nzc
 };
 
 struct StreamMaps {
-    CUtensorMap u;    // u^n buffer, box (TXP, TYP, 1): loads into the ring (+ L2 prefetch)
-    CUtensorMap un;   // u^{n-1}/u^{n+1} buffer, box (TX, TY, 1): L2 prefetch of u^{n-1}
+    CUtensorMap u;    // u^n buffer, box (TXP, TYP, 1): ring loads + L2 prefetch
+    CUtensorMap un;   // u^{n-1}/u^{n+1} buffer, box (TX, TY, 1)
     CUtensorMap b;    // model layout, box (TX, TY, 1)
-    CUtensorMap a;    // model layout, box (TX, TY, 1) (unused without damping)
+    CUtensorMap a;    // model layout, box (TX, TY, 1) (b again when there is no damping)
+};
+
+struct Ring {
+    uint32_t slot, phase;
+    __device__ __forceinline__ void advance(uint32_t n) {
+        if (++slot == n) {
+            slot = 0;
+            phase ^= 1;
+        }
+    }
 };
 
 }  // namespace
 
-template <class C>
-__global__ void __launch_bounds__(C::NTHREADS, 1)
+// One work item (xy tile, z chunk) for a consumer thread.  INTERIOR tiles need
+// no bounds predicates.  The ring positions advance exactly like the producer's.
+template <class C, bool INTERIOR, bool TEAM>
+__device__ __forceinline__ void consume_item(const StreamArgs& A, const float* ring, const float* pring,
+                                             uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
+                                             int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
+                                             Ring& rp) {
+    constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
+    const Geom& g = A.g;
+    const int nz = g.nz;
+    const int ntiles = A.ntx * A.nty;
+    const int niter = ze - zb + 2 * R;
+    const int64_t pitch = g.pitch, plane = g.plane;
+    const float2 C0 = f2(A.c.C0, A.c.C0);
+    const float2 two = f2(2.0f, 2.0f), one = f2(1.0f, 1.0f);
+    const int xa = x0 + lane, xb = x0 + lane + 32;
+    const bool inA = INTERIOR || xa < g.nx, inB = INTERIOR || xb < g.nx;
+    bool ok_a[RY], ok_b[RY];
+#pragma unroll
+    for (int i = 0; i < RY; ++i) {
+        const bool r = INTERIOR || (y0 + ly + i) < g.ny;
+        ok_a[i] = inA && r;
+        ok_b[i] = inB && r;
+    }
+    // u^{n+1} of (z, y0+ly, xa): advanced by `plane` per output plane
+    float* outp = A.unext + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
+    const uint8_t* fl = A.flags + (int64_t)zb * ntiles + tile;
+
+    float2 q[RY][Q];
+#pragma unroll
+    for (int i = 0; i < RY; ++i)
+#pragma unroll
+        for (int j = 0; j < Q; ++j) q[i][j] = f2(0.0f, 0.0f);
+
+    for (int kb = 0; kb < niter; kb += Q) {
+#pragma unroll
+        for (int uq = 0; uq < Q; ++uq) {
+            const int k = kb + uq;
+            if (k >= niter) break;
+            mbar_wait(&fullU[ru.slot], ru.phase);
+            const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + lane;
+            // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
+#pragma unroll
+            for (int i = 0; i < RY; ++i) q[i][uq] = f2(P[i * TXP], P[i * TXP + 32]);
+            const uint32_t slotR = ru.slot >= (uint32_t)R ? ru.slot - R : ru.slot + SU - R;  // plane p-R
+            if (k >= 2 * R) {
+                const int z = zb + k - 2 * R;  // output plane
+                const float* Qs = ring + slotR * C::STAGE_STRIDE_F + ly * TXP + RP + lane;
+                // (u^{n-1}, b, a) tiles of the output plane
+                mbar_wait(&fullP[rp.slot], rp.phase);
+                const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + lane;
+                const bool use_a = A.a != nullptr && fl[(int64_t)(z - zb) * ntiles];
+                // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
+                float2 col[RY + 2 * R];
+#pragma unroll
+                for (int r = 0; r < RY + 2 * R; ++r) col[r] = f2(Qs[r * TXP], Qs[r * TXP + 32]);
+                float2 res[RY];
+#pragma unroll
+                for (int i = 0; i < RY; ++i) {
+                    const float* row = Qs + (i + R) * TXP;
+                    const float2 uc = q[i][(uq + Q - R) % Q];
+                    float2 L = mul2(C0, uc);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        L = fma2(f2(A.c.C[2][j], A.c.C[2][j]),
+                                 add2(f2(row[-j], row[32 - j]), f2(row[j], row[32 + j])), L);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        L = fma2(f2(A.c.C[1][j], A.c.C[1][j]), add2(col[i + R - j], col[i + R + j]), L);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+                        L = fma2(f2(A.c.C[0][j], A.c.C[0][j]),
+                                 add2(q[i][(uq + Q - R - j) % Q], q[i][(uq + Q - R + j) % Q]), L);
+                    const float* pr = Pp + i * TX;
+                    const float2 um = f2(pr[0], pr[32]);
+                    const float2 bb = f2(pr[C::PTILE_FLOATS], pr[C::PTILE_FLOATS + 32]);
+                    const float2 aa = use_a ? f2(pr[2 * C::PTILE_FLOATS], pr[2 * C::PTILE_FLOATS + 32]) : one;
+                    // t = 2u - u^{n-1} (2u exact: one rounding), w = fma(b, L, t)
+                    const float2 t = fma2(two, uc, f2(-um.x, -um.y));
+                    const float2 wv = fma2(bb, L, t);
+                    const float2 rr = mul2(add2(one, f2(-aa.x, -aa.y)), um);
+                    const float2 un = fma2(aa, wv, rr);
+                    float* o = outp + i * pitch;
+                    if (ok_a[i]) o[0] = un.x;
+                    if (ok_b[i]) o[32] = un.y;
+                    res[i] = un;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyP[rp.slot]);
+                rp.advance(SP);
+                if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
+                    // fused exchange: boundary planes also go straight into the neighbour's halo
+                    const int64_t om = (outp - A.unext) - (int64_t)R * plane;  // model-layout index
+                    float* h = (A.lo && z < R) ? A.lo + A.lo_off + om
+                                               : A.hi + A.hi_off + om - (int64_t)(nz - R) * plane;
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) {
+                        if (ok_a[i]) h[i * pitch] = res[i].x;
+                        if (ok_b[i]) h[i * pitch + 32] = res[i].y;
+                    }
+                }
+                outp += plane;
+            }
+            // release the stage of plane p - R (no longer needed by any later output)
+            if (k >= R) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyU[slotR]);
+            }
+            ru.advance(SU);
+        }
+    }
+    // release the last R stages of this item (planes ze .. ze+R-1)
+#pragma unroll 1
+    for (int m = 0; m < R; ++m) {
+        const uint32_t s = ru.slot >= (uint32_t)(R - m) ? ru.slot - (R - m) : ru.slot + SU - (R - m);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyU[s]);
+    }
+}
+
+template <class C, bool TEAM>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     stream_kernel(const __grid_constant__ StreamMaps M, const __grid_constant__ StreamArgs A) {
-    constexpr int R = C::R, TX = C::TX, RY = C::RY, RP = C::RP, TXP = C::TXP, SU = C::SU, PD = C::PD;
+    constexpr int R = C::R, TX = C::TX, TY = C::TY, RP = C::RP, SU = C::SU, SP = C::SP, PD = C::PD, DP = C::DP;
     extern __shared__ __align__(128) unsigned char smem[];
     float* ring = reinterpret_cast<float*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)SU * C::STAGE_STRIDE);
-    uint64_t* empty = full + SU;
+    float* pring = reinterpret_cast<float*>(smem + C::U_BYTES);
+    uint64_t* fullU = reinterpret_cast<uint64_t*>(smem + C::U_BYTES + C::P_BYTES);
+    uint64_t* emptyU = fullU + SU;
+    uint64_t* fullP = emptyU + SU;
+    uint64_t* emptyP = fullP + SP;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
+    const int lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < SU; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], C::NWARPS_COMP);
+            mbar_init(&fullU[s], 1);
+            mbar_init(&emptyU[s], C::NWARPS_COMP);
+        }
+        for (int s = 0; s < SP; ++s) {
+            mbar_init(&fullP[s], 1);
+            mbar_init(&emptyP[s], C::NWARPS_COMP);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -151,147 +307,76 @@ __global__ void __launch_bounds__(C::NTHREADS, 1)
     const Geom& g = A.g;
     const int nz = g.nz;
     const int ntiles = A.ntx * A.nty;
-    const int64_t w_begin = (int64_t)blockIdx.x * A.per;
-    const int64_t w_end = min(A.total, w_begin + A.per);
-    if (w_begin >= w_end) return;
 
-    if (warp == C::NWARPS_COMP) {
-        // ---------------- producer warp ----------------
-        // TMA loads of u^n plane tiles (with halo) into the ring, D planes ahead of the
-        // consumers, and L2 prefetches PD planes ahead of everything the consumers stream
-        // (u^n tiles, and u^{n-1}, b, a tiles of the output planes).
-        if ((tid & 31) == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.u) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.un) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&M.b) : "memory");
-            if (A.a) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.a) : "memory");
-            uint32_t it = 0;
-            for (int64_t w = w_begin; w < w_end;) {
-                const int tile = (int)(w / nz);
-                const int zb = (int)(w % nz);
-                const int ze = (int)((int64_t)nz < zb + (w_end - w) ? (int64_t)nz : zb + (w_end - w));
-                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * C::TY;
+    if (warp >= C::NWARPS_COMP) {
+        // ---------------- producer warps ----------------
+        // warp NWARPS_COMP: u^n plane tiles (with halo) into the ring, D planes ahead, and L2
+        // prefetches PD planes ahead; warp NWARPS_COMP+1: the u^{n-1}, b, a tiles of the output
+        // planes into the streams ring, DP planes ahead (+ their L2 prefetches).
+        const bool is_u = warp == C::NWARPS_COMP;
+        if (lane == 0) {
+            if (is_u) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.u) : "memory");
+            } else {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.un) : "memory");
+                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.b) : "memory");
+                if (A.a) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.a) : "memory");
+            }
+            Ring rr{0, 0};
+            for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+                const int tile = item % ntiles;
+                const int zb = (item / ntiles) * A.zc;
+                const int ze = min(nz, zb + A.zc);
+                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
                 const int niter = ze - zb + 2 * R;
-                auto l2_prefetch = [&](int kk) {
-                    // u^n plane zb-R+kk (buffer plane zb+kk) and the output plane zb-2R+kk's streams
-                    if (kk < niter) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + kk);
-                    const int zo = zb - 2 * R + kk;
-                    if (zo >= zb && zo < ze) {
-                        tma_prefetch_l2_3d(&M.un, x0, y0, zo + R);
-                        tma_prefetch_l2_3d(&M.b, x0, y0, zo);
-                        if (A.a && A.flags[(int64_t)zo * ntiles + tile]) tma_prefetch_l2_3d(&M.a, x0, y0, zo);
+                if (is_u) {
+                    for (int kk = 0; kk < PD && kk < niter; ++kk) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + kk);
+                    for (int k = 0; k < niter; ++k) {
+                        if (k + PD < niter) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + k + PD);
+                        mbar_wait(&emptyU[rr.slot], rr.phase ^ 1);
+                        mbar_expect_tx(&fullU[rr.slot], C::STAGE_BYTES);
+                        tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, &M.u, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
+                        rr.advance(SU);
                     }
-                };
-                for (int kk = 0; kk < PD; ++kk) l2_prefetch(kk);
-                for (int k = 0; k < niter; ++k, ++it) {
-                    l2_prefetch(k + PD);
-                    const int s = it % SU;
-                    const uint32_t ph = (it / SU) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], C::STAGE_BYTES);
-                    // plane p = zb - R + k lives at buffer plane p + R
-                    tma_load_3d(ring + (size_t)s * C::STAGE_STRIDE_F, &M.u, &full[s], x0 - RP, y0 - R, zb + k);
+                } else {
+                    auto l2_prefetch = [&](int z) {
+                        if (z >= ze) return;
+                        tma_prefetch_l2_3d(&M.un, x0, y0, z + R);
+                        tma_prefetch_l2_3d(&M.b, x0, y0, z);
+                        if (A.a && A.flags[(int64_t)z * ntiles + tile]) tma_prefetch_l2_3d(&M.a, x0, y0, z);
+                    };
+                    for (int z = zb; z < zb + PD; ++z) l2_prefetch(z);
+                    for (int z = zb; z < ze; ++z) {
+                        l2_prefetch(z + PD);
+                        const bool use_a = A.a && A.flags[(int64_t)z * ntiles + tile];
+                        float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
+                        mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
+                        mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
+                        tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
+                        tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
+                        if (use_a) tma_load_3d(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z);
+                        rr.advance(SP);
+                    }
                 }
-                w += ze - zb;
             }
         }
         return;
     }
 
     // ---------------- consumer warps ----------------
-    const int lx = tid % TX;
-    const int ly = (tid / TX) * RY;
-    const float C0 = A.c.C0;
-    uint32_t it = 0;
-    for (int64_t w = w_begin; w < w_end;) {
-        const int tile = (int)(w / nz);
-        const int zb = (int)(w % nz);
-        const int ze = (int)((int64_t)nz < zb + (w_end - w) ? (int64_t)nz : zb + (w_end - w));
-        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * C::TY;
-        const int x = x0 + lx;
-        const bool xin = x < g.nx;
-        const int niter = ze - zb + 2 * R;
-
-        float q[RY][2 * R + 1];
-#pragma unroll
-        for (int i = 0; i < RY; ++i)
-#pragma unroll
-            for (int j = 0; j <= 2 * R; ++j) q[i][j] = 0.0f;
-        // streams of the next output plane (L2 hits: the producer prefetched them)
-        float pu[RY], pb[RY], pa[RY];
-        auto fetch = [&](int z) {
-            const bool use_a = A.a != nullptr && A.flags[(int64_t)z * ntiles + tile];
-#pragma unroll
-            for (int i = 0; i < RY; ++i) {
-                const int y = y0 + ly + i;
-                const bool in = xin && y < g.ny;
-                const int64_t o = (int64_t)z * g.plane + (int64_t)y * g.pitch + x;
-                pu[i] = in ? ldg_stream(A.unext + o + (int64_t)R * g.plane) : 0.0f;
-                pb[i] = in ? ldg_stream(A.b + o) : 0.0f;
-                pa[i] = (in && use_a) ? ldg_stream(A.a + o) : 1.0f;
-            }
-        };
-        fetch(zb);
-
-        for (int k = 0; k < niter; ++k, ++it) {
-            const int s = it % SU;
-            const uint32_t ph = (it / SU) & 1;
-            mbar_wait(&full[s], ph);
-            const float* P = ring + (size_t)s * C::STAGE_STRIDE_F;
-            // shift the z queue and append the centre values of the newest plane
-#pragma unroll
-            for (int i = 0; i < RY; ++i) {
-#pragma unroll
-                for (int j = 0; j < 2 * R; ++j) q[i][j] = q[i][j + 1];
-                q[i][2 * R] = P[(ly + i + R) * TXP + lx + RP];
-            }
-            if (k >= 2 * R) {
-                const int z = zb + k - 2 * R;  // output plane; its stage is R iterations old
-                const float* Q = ring + (size_t)((it - R) % SU) * C::STAGE_STRIDE_F;
-                // column of the output plane: rows ly .. ly+RY-1+2R at this x
-                float col[RY + 2 * R];
-#pragma unroll
-                for (int r = 0; r < RY + 2 * R; ++r) col[r] = Q[(ly + r) * TXP + lx + RP];
-#pragma unroll
-                for (int i = 0; i < RY; ++i) {
-                    const float* row = Q + (ly + i + R) * TXP + lx + RP;
-                    const float uc = q[i][R];
-                    float L = __fmul_rn(C0, uc);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j) L = __fmaf_rn(A.c.C[2][j], __fadd_rn(row[-j], row[j]), L);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = __fmaf_rn(A.c.C[1][j], __fadd_rn(col[i + R - j], col[i + R + j]), L);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = __fmaf_rn(A.c.C[0][j], __fadd_rn(q[i][R - j], q[i][R + j]), L);
-                    const float t = __fsub_rn(__fmul_rn(2.0f, uc), pu[i]);
-                    const float wv = __fmaf_rn(pb[i], L, t);
-                    const float rr = __fmul_rn(__fsub_rn(1.0f, pa[i]), pu[i]);
-                    const float un = __fmaf_rn(pa[i], wv, rr);
-                    const int y = y0 + ly + i;
-                    if (xin && y < g.ny) {
-                        const int64_t o = (int64_t)z * g.plane + (int64_t)y * g.pitch + x;
-                        A.unext[o + (int64_t)R * g.plane] = un;
-                        if (A.lo && z < R) A.lo[A.lo_off + o] = un;
-                        if (A.hi && z >= nz - R) A.hi[A.hi_off + o - (int64_t)(nz - R) * g.plane] = un;
-                    }
-                }
-                if (z + 1 < ze) fetch(z + 1);
-            }
-            // release the stage of plane p - R (no longer needed by any later output)
-            if (k >= R) {
-                __syncwarp();
-                if ((tid & 31) == 0) mbar_arrive(&empty[(it - R) % SU]);
-            }
-        }
-        // release the last R stages of this segment (planes ze .. ze+R-1)
-#pragma unroll 1
-        for (int k = niter - R; k < niter; ++k) {
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[(it - (niter - k)) % SU]);
-        }
-        w += ze - zb;
+    const int ly = warp * C::RY;  // first tile row of this thread
+    Ring ru{0, 0}, rp{0, 0};
+    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+        const int tile = item % ntiles;
+        const int zb = (item / ntiles) * A.zc;
+        const int ze = min(nz, zb + A.zc);
+        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+        if (x0 + TX <= g.nx && y0 + TY <= g.ny)
+            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, tile, zb, ze, x0, y0, lane, ly,
+                                        ru, rp);
+        else
+            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, tile, zb, ze, x0, y0, lane,
+                                         ly, ru, rp);
     }
 }
 
@@ -331,6 +416,7 @@ struct StreamPlan {
     size_t smem = 0;
     int nthreads = 0;
     int TX = 0, TY = 0;
+    int nzc = 1, zc = 0;
 };
 
 namespace {
@@ -354,8 +440,9 @@ cudaError_t encode3d(CUtensorMap* m, const void* base, const Geom& g, int planes
     cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
     cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
     cuuint32_t estr[3] = {1, 1, 1};
+    // no L2 promotion: a promoted halo'd box fetches whole 256-B segments of the neighbours
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -366,10 +453,17 @@ cudaError_t setup(StreamPlan* p, const Geom& g) {
     p->nthreads = C::NTHREADS;
     p->TX = C::TX;
     p->TY = C::TY;
-    cudaError_t e = cudaFuncSetAttribute(stream_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(stream_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::SMEM);
     if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<C>, C::NTHREADS, C::SMEM);
+    e = cudaFuncSetAttribute(stream_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    int occ = 0, occ_t = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<C, false>, C::NTHREADS, C::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, stream_kernel<C, true>, C::NTHREADS, C::SMEM);
+    if (e != cudaSuccess) return e;
+    occ = occ < occ_t ? occ : occ_t;
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorNotSupported;
     int dev = 0, sms = 0;
@@ -399,7 +493,6 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.g = g;
     A.c = c;
     A.unext = unext;
-    A.b = b;
     A.a = a;
     A.flags = p->flags;
     A.lo = halo.lo[parity_next];
@@ -408,21 +501,35 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.hi_off = halo.hi_off;
     A.ntx = p->ntx;
     A.nty = p->nty;
-    A.total = (int64_t)p->ntx * p->nty * g.nz;
-    A.per = (A.total + p->grid - 1) / p->grid;
-    stream_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
+    A.nzc = p->nzc;
+    A.zc = p->zc;
+    A.nitems = p->ntx * p->nty * p->nzc;
+    if (A.lo || A.hi)
+        stream_kernel<C, true><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
+    else
+        stream_kernel<C, false><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
     return cudaGetLastError();
 }
 
-// configuration table: (R, TX, TY, RY, D = ring lookahead, PD = L2 prefetch distance)
-using C1 = Cfg<1, 64, 16, 4, 2, 6>;
-using C2 = Cfg<2, 64, 16, 4, 2, 6>;
-using C3 = Cfg<3, 64, 16, 4, 2, 6>;
-using C4 = Cfg<4, 64, 16, 4, 2, 6>;
-using C5 = Cfg<5, 64, 16, 4, 2, 6>;
-using C6 = Cfg<6, 64, 16, 4, 2, 6>;
-using C7 = Cfg<7, 64, 16, 4, 2, 6>;
-using C8 = Cfg<8, 64, 16, 4, 2, 6>;
+// configuration table: (R, TY, RY, D = u^n ring lookahead, DP = streams lookahead,
+//                       PD = L2 prefetch distance, min CTAs/SM)
+using C1 = Cfg<1, 16, 2, 2, 2, 6, 2>;
+using C2 = Cfg<2, 16, 2, 2, 2, 6, 2>;
+using C3 = Cfg<3, 32, 4, 2, 2, 6, 1>;
+using C4 = Cfg<4, 32, 4, 2, 2, 6, 1>;
+using C5 = Cfg<5, 32, 4, 2, 2, 6, 1>;
+using C6 = Cfg<6, 32, 4, 2, 2, 6, 1>;
+using C7 = Cfg<7, 16, 2, 2, 2, 6, 1>;
+using C8 = Cfg<8, 16, 2, 2, 2, 6, 1>;
+// development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for tile-shape measurements
+using C4v1 = Cfg<4, 32, 4, 2, 3, 6, 1>;
+using C4v2 = Cfg<4, 32, 4, 3, 3, 8, 1>;
+using C4v3 = Cfg<4, 32, 4, 2, 4, 8, 1>;
+
+int variant() {
+    const char* v = getenv("AW_STREAM_VARIANT");
+    return v ? atoi(v) : 0;
+}
 
 }  // namespace
 
@@ -431,7 +538,12 @@ using C8 = Cfg<8, 64, 16, 4, 2, 6>;
         case 1: { using C = C1; EXPR; } break; \
         case 2: { using C = C2; EXPR; } break; \
         case 3: { using C = C3; EXPR; } break; \
-        case 4: { using C = C4; EXPR; } break; \
+        case 4:                            \
+            if (variant() == 1) { using C = C4v1; EXPR; } \
+            else if (variant() == 2) { using C = C4v2; EXPR; } \
+            else if (variant() == 3) { using C = C4v3; EXPR; } \
+            else { using C = C4; EXPR; } \
+            break;                         \
         case 5: { using C = C5; EXPR; } break; \
         case 6: { using C = C6; EXPR; } break; \
         case 7: { using C = C7; EXPR; } break; \
@@ -453,14 +565,21 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     }
     p->ntx = (g.nx + p->TX - 1) / p->TX;
     p->nty = (g.ny + p->TY - 1) / p->TY;
-    const int64_t nflags = (int64_t)p->ntx * p->nty * g.nz;
+    // z chunks: enough items that the cyclic hand-out balances to ~1-2% (>= 16 items per CTA
+    // when possible), chunks no thinner than 4R planes (warm-up overhead 2R/zc)
+    const int ntiles = p->ntx * p->nty;
+    int nzc = 1;
+    while ((int64_t)ntiles * nzc < 16LL * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
+    p->zc = (g.nz + nzc - 1) / nzc;
+    p->nzc = (g.nz + p->zc - 1) / p->zc;
+    const int64_t nflags = (int64_t)ntiles * g.nz;
     e = cudaMalloc(&p->flags, nflags);
     if (e != cudaSuccess) {
         delete p;
         return e;
     }
     if (a) {
-        dim3 grid(p->ntx * p->nty, g.nz);
+        dim3 grid(ntiles, g.nz);
         eta_flags_kernel<<<grid, 256, 0, s>>>(g, a, p->TX, p->TY, p->ntx, p->nty, p->flags);
         unsigned long long* cnt = nullptr;
         e = cudaMallocAsync(&cnt, sizeof(unsigned long long), s);
