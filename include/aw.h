@@ -208,6 +208,12 @@ int aw_abi_version(void);
  * handshake per step (no separate copy kernel, no host round trip).
  * ------------------------------------------------------------------------ */
 
+/* Host-only: the slab [*z0, *z0 + *nz) of axis 0 that rank `rank` of `world`
+ * owns for a grid of n0 planes (nearly equal split, the first n0 % world ranks
+ * get one more plane).  AW_EINVAL if a slab would be thinner than k/2 = R
+ * planes (the exchange reaches only the direct neighbours). */
+aw_status aw_slab_partition(int64_t n0, int world, int rank, int R, int64_t* z0, int64_t* nz);
+
 /* Bytes of the opaque export record of one rank (cudaIpc handles + offsets). */
 size_t aw_team_export_size(void);
 /* Write this rank's export record into out[aw_team_export_size()]. */

@@ -68,6 +68,7 @@ _SIGS = {
     "aw_critical_dt": (_D, [_I, _P, _I, _D]),
     "aw_last_error": (ctypes.c_char_p, []),
     "aw_abi_version": (_I, []),
+    "aw_slab_partition": (_S, [_I64, _I, _I, _I, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "aw_team_export_size": (ctypes.c_size_t, []),
     "aw_team_export": (_S, [_P, _P]),
     "aw_team_connect": (_S, [_P, _P]),
@@ -249,6 +250,13 @@ class Grid:
 def critical_dt(spacing, space_order, vmax):
     sp = (ctypes.c_double * len(spacing))(*[float(s) for s in spacing])
     return aw_critical_dt(len(spacing), ctypes.cast(sp, _P), int(space_order), float(vmax))
+
+
+def slab_partition(n0, world, rank, radius):
+    """(z0, nz): the planes of axis 0 rank `rank` of `world` owns (host-only C call)."""
+    z0, nz = _I64(), _I64()
+    check(aw_slab_partition(int(n0), int(world), int(rank), int(radius), ctypes.byref(z0), ctypes.byref(nz)))
+    return z0.value, nz.value
 
 
 def team_connect_local(grids):

@@ -639,11 +639,11 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
     }
     if (device >= ndev) return fail(AW_EINVAL, "device %d >= device count %d", device, ndev);
     // slab of axis 0: nearly equal split
-    const int64_t n0 = shape[0];
-    const int64_t base = n0 / world, rem = n0 % world;
-    const int64_t nz = base + (rank < rem ? 1 : 0);
-    const int64_t z0 = rank * base + std::min<int64_t>(rank, rem);
-    if (world > 1 && nz < R) return fail(AW_EINVAL, "slab of %lld planes is thinner than k/2=%d", (long long)nz, R);
+    int64_t z0 = 0, nz = 0;
+    {
+        aw_status pst = aw_slab_partition(shape[0], world, rank, R, &z0, &nz);
+        if (pst) return pst;
+    }
 
     aw_grid* g = new aw_grid();
     g->ndim = ndim;
@@ -1069,6 +1069,17 @@ struct aw_team_record {
 };
 
 size_t aw_team_export_size(void) { return sizeof(aw_team_record); }
+
+aw_status aw_slab_partition(int64_t n0, int world, int rank, int R, int64_t* z0, int64_t* nz) {
+    if (n0 < 1 || world < 1 || rank < 0 || rank >= world || R < 1 || !z0 || !nz)
+        return fail(AW_EINVAL, "bad slab partition arguments");
+    const int64_t base = n0 / world, rem = n0 % world;
+    const int64_t n = base + (rank < rem ? 1 : 0);
+    if (world > 1 && n < R) return fail(AW_EINVAL, "slab of %lld planes is thinner than k/2=%d", (long long)n, R);
+    *z0 = rank * base + std::min<int64_t>(rank, rem);
+    *nz = n;
+    return AW_OK;
+}
 
 aw_status aw_team_export(aw_grid* g, void* out) {
     CHECK_STATE(g);

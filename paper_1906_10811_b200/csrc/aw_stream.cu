@@ -117,7 +117,8 @@ struct Cfg {
     static constexpr int PSTAGE_FLOATS = 3 * PTILE_FLOATS;  // u^{n-1}, b, a
     static constexpr size_t U_BYTES = (size_t)SU * STAGE_STRIDE;
     static constexpr size_t P_BYTES = (size_t)SP * PSTAGE_FLOATS * 4;
-    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t);
+    // + full/empty barriers of both rings + one "stage carries a" word per streams stage
+    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + SP * sizeof(int);
     static_assert(TY % RY == 0, "tile shape");
     static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
 };
@@ -161,6 +162,7 @@ struct Ring {
 template <class C, bool INTERIOR, bool TEAM>
 __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* ring, const float* pring,
                                              uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
+                                             const volatile int* pflag,
                                              int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
                                              Ring& rp) {
     constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
@@ -182,7 +184,6 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
     }
     // u^{n+1} of (z, y0+ly, xa): advanced by `plane` per output plane
     float* outp = A.unext + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
-    const uint8_t* fl = A.flags + (int64_t)zb * ntiles + tile;
 
     float2 q[RY][Q];
 #pragma unroll
@@ -207,7 +208,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                 // (u^{n-1}, b, a) tiles of the output plane
                 mbar_wait(&fullP[rp.slot], rp.phase);
                 const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + lane;
-                const bool use_a = A.a != nullptr && fl[(int64_t)(z - zb) * ntiles];
+                const bool use_a = pflag[rp.slot] != 0;  // set by the streams producer before its arrive
                 // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
                 float2 col[RY + 2 * R];
 #pragma unroll
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     uint64_t* emptyU = fullU + SU;
     uint64_t* fullP = emptyU + SU;
     uint64_t* emptyP = fullP + SP;
+    int* pflag = reinterpret_cast<int*>(emptyP + SP);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -351,6 +353,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         const bool use_a = A.a && A.flags[(int64_t)z * ntiles + tile];
                         float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
                         mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
+                        pflag[rr.slot] = use_a;  // published by the release of the arrive below
                         mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
                         tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
                         tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
@@ -372,10 +375,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         const int ze = min(nz, zb + A.zc);
         const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
         if (x0 + TX <= g.nx && y0 + TY <= g.ny)
-            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, tile, zb, ze, x0, y0, lane, ly,
+            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pflag, tile, zb, ze, x0, y0, lane, ly,
                                         ru, rp);
         else
-            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, tile, zb, ze, x0, y0, lane,
+            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pflag, tile, zb, ze, x0, y0, lane,
                                          ly, ru, rp);
     }
 }
