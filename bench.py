@@ -252,12 +252,8 @@ def main():
     if args.kernel != "auto":
         g.set_option(aw.AW_OPT_KERNEL, {"v1": aw.AW_KERNEL_V1, "stream": aw.AW_KERNEL_STREAM}[args.kernel])
     if world > 1:
-        rec_bytes = g.team_export()
-        t = torch.frombuffer(bytearray(rec_bytes), dtype=torch.uint8).to(device)
-        allt = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        g.team_connect(b"".join(bytes(x.cpu().numpy().tobytes()) for x in allt))
-        dist.barrier()
+        from paper_1906_10811_b200 import team
+        team.connect(g)  # cudaIpc records all-gathered in rank order -> aw_team_connect
 
     import workloads as W
     m_dev, d_dev = local_model(spec, g.z0, g.nz, device)
