@@ -516,18 +516,18 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
 
 // configuration table: (R, TY, RY, D = u^n ring lookahead, DP = streams lookahead,
 //                       PD = L2 prefetch distance, min CTAs/SM)
-using C1 = Cfg<1, 16, 2, 2, 2, 6, 2>;
-using C2 = Cfg<2, 16, 2, 2, 2, 6, 2>;
-using C3 = Cfg<3, 32, 4, 2, 2, 6, 1>;
-using C4 = Cfg<4, 32, 4, 2, 2, 6, 1>;
-using C5 = Cfg<5, 32, 4, 2, 2, 6, 1>;
-using C6 = Cfg<6, 32, 4, 2, 2, 6, 1>;
-using C7 = Cfg<7, 16, 2, 2, 2, 6, 1>;
-using C8 = Cfg<8, 16, 2, 2, 2, 6, 1>;
-// development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for tile-shape measurements
-using C4v1 = Cfg<4, 32, 4, 2, 3, 6, 1>;
-using C4v2 = Cfg<4, 32, 4, 3, 3, 8, 1>;
-using C4v3 = Cfg<4, 32, 4, 2, 4, 8, 1>;
+using C1 = Cfg<1, 32, 4, 4, 4, 0, 1>;
+using C2 = Cfg<2, 32, 4, 4, 4, 0, 1>;
+using C3 = Cfg<3, 32, 4, 4, 4, 0, 1>;
+using C4 = Cfg<4, 32, 4, 4, 4, 0, 1>;
+using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
+using C6 = Cfg<6, 32, 4, 2, 3, 0, 1>;
+using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
+using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
+// development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
+using C4v1 = Cfg<4, 32, 4, 4, 3, 0, 1>;
+using C4v2 = Cfg<4, 32, 4, 2, 2, 6, 1>;  // round-1 v4 (L2 prefetch 6 planes ahead)
+using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
 
 int variant() {
     const char* v = getenv("AW_STREAM_VARIANT");
