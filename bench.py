@@ -22,6 +22,7 @@ roofline: stencil kernel, 16 algorithmic B/point-update over
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -267,15 +268,21 @@ def main():
         if world > 1:
             dist.barrier()
 
+    verbose = bool(os.environ.get("AW_BENCH_VERBOSE"))
+
     def one_step(m, d, wv, traces):
-        barrier()  # team calls: neighbours finished the previous run before anyone resets
-        g.reset()
-        g.set_model(m, d, aw.AW_LOCAL)
-        g.add_sources(spec["src"], wv)
-        g.add_receivers(spec["rec"], nt)
-        barrier()
-        g.run(nt, spec["dt"])
-        g.read_receivers(out=traces)
+        calls = (("barrier", barrier), ("reset", g.reset), ("set_model", lambda: g.set_model(m, d, aw.AW_LOCAL)),
+                 ("add_sources", lambda: g.add_sources(spec["src"], wv)),
+                 ("add_receivers", lambda: g.add_receivers(spec["rec"], nt)), ("barrier", barrier),
+                 ("run", lambda: g.run(nt, spec["dt"])), ("read_receivers", lambda: g.read_receivers(out=traces)))
+        # team calls: the first barrier makes sure the neighbours finished the previous run before
+        # anyone resets; the second that everyone is set up before the collective run
+        for name, fn in calls:
+            t0 = time.perf_counter()
+            fn()
+            dt_ms = 1e3 * (time.perf_counter() - t0)
+            if verbose and (dt_ms > 20 and name != "run"):
+                print(f"  slow call {name}: {dt_ms:.1f} ms", file=sys.stderr, flush=True)
 
     # per-launch CUDA events around the stencil kernel (the event pool is created in the warm-up)
     g.set_option(aw.AW_OPT_TIMING, 1)
@@ -287,6 +294,8 @@ def main():
     launches0 = g.stats()["launches_total"]
     torch.cuda.synchronize()
     barrier()
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region
     if not os.environ.get("AW_BENCH_NO_CLOCKS"):
         clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -306,6 +315,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    gc.enable()
     ms = ev0.elapsed_time(ev1)
     launches = g.stats()["launches_total"] - launches0
     st = g.stats()

@@ -174,6 +174,11 @@ struct aw_grid {
     // stats
     aw_run_stats stats{};
     int64_t launch_count = 0;  // kernels launched since creation
+    // device arenas of the sparse data (grown, never shrunk: no allocation in steady state)
+    char* src_arena = nullptr;
+    size_t src_cap = 0;
+    char* rec_arena = nullptr;
+    size_t rec_cap = 0;
 };
 
 namespace {
@@ -299,26 +304,26 @@ unsigned long long enc(const aw_grid* g, int64_t level) {
 }
 bool team_mode(const aw_grid* g) { return g->world > 1; }
 
-void free_sources(aw_grid* g) {
-    dfree(g->d_wavelet);
-    dfree(g->d_inj_off);
-    dfree(g->d_inj_plane);
-    dfree(g->d_inj_ptr);
-    dfree(g->d_inj_src);
-    dfree(g->d_inj_moff);
-    dfree(g->d_inj_w64);
-    dfree(g->d_inj_s);
+void free_sources(aw_grid* g) {  // the device arrays are views into g->src_arena
+    g->d_wavelet = nullptr;
+    g->d_inj_off = nullptr;
+    g->d_inj_plane = nullptr;
+    g->d_inj_ptr = nullptr;
+    g->d_inj_src = nullptr;
+    g->d_inj_moff = nullptr;
+    g->d_inj_w64 = nullptr;
+    g->d_inj_s = nullptr;
     g->ns = g->src_nt = g->nuc = g->nent = 0;
     g->src_corner_lin.clear();
     g->src_w64.clear();
     g->ent_src.clear();
     g->ent_beta.clear();
 }
-void free_receivers(aw_grid* g) {
-    dfree(g->d_rec_id);
-    dfree(g->d_rec_off);
-    dfree(g->d_rec_w);
-    dfree(g->d_traces);
+void free_receivers(aw_grid* g) {  // views into g->rec_arena
+    g->d_rec_id = nullptr;
+    g->d_rec_off = nullptr;
+    g->d_rec_w = nullptr;
+    g->d_traces = nullptr;
     g->nr = g->rec_nt = g->nrl = 0;
     g->rec_corner_lin.clear();
     g->rec_w32.clear();
@@ -330,6 +335,43 @@ aw_status upload(aw_grid* g, T** dst, const std::vector<T>& v) {
     if (v.empty()) return AW_OK;
     CK(cudaMalloc((void**)dst, v.size() * sizeof(T)));
     CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g->s));
+    return AW_OK;
+}
+
+// Packs several host arrays into one device arena (16-B aligned slices) with a single copy.
+struct Packer {
+    std::vector<char> host;
+    size_t off = 0;
+    template <class T>
+    size_t add(const std::vector<T>& v) {  // returns the slice offset
+        size_t o = off;
+        off = (off + v.size() * sizeof(T) + 15) / 16 * 16;
+        host.resize(off);
+        if (!v.empty()) std::memcpy(host.data() + o, v.data(), v.size() * sizeof(T));
+        return o;
+    }
+    size_t reserve(size_t bytes) {  // uninitialised slice (filled on the device)
+        size_t o = off;
+        off = (off + bytes + 15) / 16 * 16;
+        return o;
+    }
+};
+
+aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes) {
+    if (*cap >= bytes && *arena) return AW_OK;
+    if (*arena) {
+        CK(cudaStreamSynchronize(g->s));
+        cudaFree(*arena);
+        *arena = nullptr;
+        *cap = 0;
+    }
+    size_t want = bytes + bytes / 2 + 256;
+    cudaError_t e = cudaMalloc((void**)arena, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? AW_ENOMEM : AW_ECUDA, "sparse arena: %s", cudaGetErrorString(e));
+    }
+    *cap = want;
     return AW_OK;
 }
 
@@ -361,19 +403,23 @@ aw_status prepare(aw_grid* g, double dt) {
     CK(aw::launch_source_scales(g->m, g->have_damp ? g->eta : nullptr, g->d_inj_moff, g->d_inj_w64, g->d_inj_s,
                                 g->nent, dt, g->s));
     g->launch_count += 1 + (g->nent > 0 ? 1 : 0);
-    if (g->plan) {
+    const bool want_stream = g->opt_kernel != AW_KERNEL_V1 && g->ndim == 3;
+    if (g->plan && !want_stream) {
         aw::stream_release(g->plan);
         g->plan = nullptr;
     }
     g->kernel_used = AW_KERNEL_V1;
     g->eta_tiles_pct = g->have_damp ? 100 : 0;
-    if (g->opt_kernel != AW_KERNEL_V1 && g->ndim == 3) {
+    if (want_stream) {
         const float* ub[2] = {g->ubuf[0], g->ubuf[1]};
-        cudaError_t e = aw::stream_prepare(g->geom, ub, g->b, g->have_damp ? g->a : nullptr, &g->plan,
-                                           &g->eta_tiles_pct, g->s);
+        const float* a = g->have_damp ? g->a : nullptr;
+        // the plan (tensor maps, grid, flag buffer) is built once per handle; later runs only
+        // refresh the maps and the eta flags (no allocation, no host synchronisation)
+        cudaError_t e = g->plan ? aw::stream_refresh(g->plan, g->geom, ub, g->b, a, g->s)
+                                : aw::stream_prepare(g->geom, ub, g->b, a, &g->plan, g->s);
         if (e == cudaSuccess) {
             g->kernel_used = AW_KERNEL_STREAM;
-            g->launch_count += 1;
+            g->launch_count += a ? 2 : 0;
         } else if (e == cudaErrorNotSupported) {
             cudaGetLastError();
             if (g->opt_kernel == AW_KERNEL_STREAM)
@@ -562,6 +608,7 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
     g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
     g->stats.kernel = g->kernel_used;
+    if (g->plan) g->eta_tiles_pct = aw::stream_eta_tiles_pct(g->plan);
     g->stats.eta_tiles = g->eta_tiles_pct;
     if (g->opt_timing) {
         double sum = 0.0;
@@ -724,6 +771,8 @@ void aw_grid_destroy(aw_grid* g) {
     for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
     free_sources(g);
     free_receivers(g);
+    dfree(g->src_arena);
+    dfree(g->rec_arena);
     dfree(g->ubuf[0]);
     dfree(g->ubuf[1]);
     dfree(g->m);
@@ -848,12 +897,23 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
     inj_ptr.push_back((int)ents.size());
     g->nuc = (int)inj_off.size();
     g->nent = (int)ents.size();
-    if ((st = upload(g, &g->d_inj_off, inj_off)) || (st = upload(g, &g->d_inj_plane, inj_plane)) ||
-        (st = upload(g, &g->d_inj_ptr, inj_ptr)) || (st = upload(g, &g->d_inj_src, inj_src)) ||
-        (st = upload(g, &g->d_inj_moff, inj_moff)) || (st = upload(g, &g->d_inj_w64, inj_w)))
-        return st;
-    if (g->nent > 0) CK(cudaMalloc((void**)&g->d_inj_s, g->nent * sizeof(float)));
-    CK(cudaMalloc((void**)&g->d_wavelet, (size_t)nt_max * ns * sizeof(float)));
+    Packer pk;
+    const size_t o_off = pk.add(inj_off), o_plane = pk.add(inj_plane), o_ptr = pk.add(inj_ptr),
+                 o_src = pk.add(inj_src), o_moff = pk.add(inj_moff), o_w = pk.add(inj_w);
+    const size_t small = pk.off;
+    const size_t o_s = pk.reserve((size_t)g->nent * sizeof(float));
+    const size_t o_wav = pk.reserve((size_t)nt_max * ns * sizeof(float));
+    if ((st = ensure_arena(g, &g->src_arena, &g->src_cap, pk.off))) return st;
+    char* A = g->src_arena;
+    g->d_inj_off = (int64_t*)(A + o_off);
+    g->d_inj_plane = (int*)(A + o_plane);
+    g->d_inj_ptr = (int*)(A + o_ptr);
+    g->d_inj_src = (int*)(A + o_src);
+    g->d_inj_moff = (int64_t*)(A + o_moff);
+    g->d_inj_w64 = (double*)(A + o_w);
+    g->d_inj_s = (float*)(A + o_s);
+    g->d_wavelet = (float*)(A + o_wav);
+    CK(cudaMemcpyAsync(A, pk.host.data(), small, cudaMemcpyHostToDevice, g->s));
     cudaMemcpyKind kind = ptr_kind(wavelet) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(cudaMemcpyAsync(g->d_wavelet, wavelet, (size_t)nt_max * ns * sizeof(float), kind, g->s));
     CK(cudaStreamSynchronize(g->s));
@@ -901,10 +961,17 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
         }
     }
     g->nrl = (int)ids.size();
-    if ((st = upload(g, &g->d_rec_id, ids)) || (st = upload(g, &g->d_rec_off, offs)) ||
-        (st = upload(g, &g->d_rec_w, ws)))
-        return st;
-    CK(cudaMalloc((void**)&g->d_traces, (size_t)nt_max * nr * sizeof(float)));
+    Packer pk;
+    const size_t o_id = pk.add(ids), o_off = pk.add(offs), o_w = pk.add(ws);
+    const size_t small = pk.off;
+    const size_t o_tr = pk.reserve((size_t)nt_max * nr * sizeof(float));
+    if ((st = ensure_arena(g, &g->rec_arena, &g->rec_cap, pk.off))) return st;
+    char* A = g->rec_arena;
+    g->d_rec_id = (int*)(A + o_id);
+    g->d_rec_off = (int64_t*)(A + o_off);
+    g->d_rec_w = (float*)(A + o_w);
+    g->d_traces = (float*)(A + o_tr);
+    CK(cudaMemcpyAsync(A, pk.host.data(), small, cudaMemcpyHostToDevice, g->s));
     CK(cudaMemsetAsync(g->d_traces, 0, (size_t)nt_max * nr * sizeof(float), g->s));
     CK(cudaStreamSynchronize(g->s));
     return leave(g);
@@ -1041,6 +1108,12 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
             if (value < AW_KERNEL_AUTO || value > AW_KERNEL_STREAM) return fail(AW_EINVAL, "bad kernel %lld", (long long)value);
             g->opt_kernel = (int)value;
             g->coeffs_valid = false;
+            if (g->plan) {
+                cudaStreamSynchronize(g->s);
+                aw::stream_release(g->plan);
+                g->plan = nullptr;
+            }
+            free_graphs(g);
             return AW_OK;
         case AW_OPT_TIMING:
             g->opt_timing = value != 0;

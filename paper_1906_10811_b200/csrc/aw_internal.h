@@ -84,7 +84,10 @@ cudaError_t launch_team_raise(unsigned long long* f0, unsigned long long* f1, un
 // the configuration has no streaming specialisation.
 struct StreamPlan;
 cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* b, const float* a,
-                           StreamPlan** plan, int* eta_tiles_pct, cudaStream_t s);
+                           StreamPlan** plan, cudaStream_t s);
+cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a,
+                           cudaStream_t s);
+int stream_eta_tiles_pct(const StreamPlan* p);
 void stream_release(StreamPlan* p);
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
                                   const float* ucur, float* unext, const float* b, const float* a,

@@ -18,53 +18,64 @@ namespace aw {
 // ---------------------------------------------------------------------------
 // Coefficient precompute, fp64 then one rounding to fp32.
 // ---------------------------------------------------------------------------
-__global__ void coeffs_kernel(const float* __restrict__ m, const float* __restrict__ eta,
-                              float* __restrict__ b, float* __restrict__ a, int64_t n, double dt) {
+__device__ __forceinline__ void coeff1(float m, float eta, double dt, double dt2, float& b, float& a) {
+    const double mm = (double)m;
+    const double den = __dadd_rn(mm, __dmul_rn(__dmul_rn((double)eta, dt), 0.5));
+    b = __double2float_rn(__ddiv_rn(dt2, mm));
+    a = __double2float_rn(__ddiv_rn(mm, den));
+}
+
+// n is a multiple of 4 (rows are padded to 32 floats); float4 streams, 4 points per thread-iteration.
+__global__ void coeffs_kernel(const float4* __restrict__ m, const float4* __restrict__ eta, float4* __restrict__ b,
+                              float4* __restrict__ a, int64_t n4, double dt) {
     const double dt2 = __dmul_rn(dt, dt);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double mm = (double)m[i];
-        double e = eta ? (double)eta[i] : 0.0;
-        double den = __dadd_rn(mm, __dmul_rn(__dmul_rn(e, dt), 0.5));
-        b[i] = __double2float_rn(__ddiv_rn(dt2, mm));
-        if (a) a[i] = __double2float_rn(__ddiv_rn(mm, den));
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 mm = m[i];
+        const float4 e = eta ? eta[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 bb, aa;
+        coeff1(mm.x, e.x, dt, dt2, bb.x, aa.x);
+        coeff1(mm.y, e.y, dt, dt2, bb.y, aa.y);
+        coeff1(mm.z, e.z, dt, dt2, bb.z, aa.z);
+        coeff1(mm.w, e.w, dt, dt2, bb.w, aa.w);
+        b[i] = bb;
+        if (a) a[i] = aa;
     }
 }
 
 cudaError_t launch_coeffs(const float* m, const float* eta, float* b, float* a, int64_t n, double dt,
                           cudaStream_t s) {
-    int blocks = (int)((n + 255) / 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    const int64_t n4 = n / 4;
+    int blocks = (int)((n4 + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    coeffs_kernel<<<blocks, 256, 0, s>>>(m, eta, b, a, n, dt);
+    coeffs_kernel<<<blocks, 256, 0, s>>>((const float4*)m, (const float4*)eta, (float4*)b, (float4*)a, n4, dt);
     return cudaGetLastError();
 }
 
 // Model validation: m > 0 finite, eta >= 0 finite at every owned point.
-__global__ void validate_kernel(const float* __restrict__ m, const float* __restrict__ eta, int nz, int ny,
-                                int nx, int64_t pitch, unsigned* flag) {
-    int64_t rows = (int64_t)nz * ny;
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const float* mr = m + r * pitch;
-        const float* er = eta ? eta + r * pitch : nullptr;
-        for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-            float v = mr[x];
-            bool bad = !(v > 0.0f) || !isfinite(v);
-            if (er) {
-                float e = er[x];
-                bad |= !(e >= 0.0f) || !isfinite(e);
-            }
-            if (bad) atomicOr(flag, 1u);
-        }
+// flat float4 walk over the padded arrays; x = element index mod pitch (pitch % 4 == 0)
+__global__ void validate_kernel(const float4* __restrict__ m, const float4* __restrict__ eta, int64_t n4, int nx,
+                                int64_t pitch, unsigned* flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)((4 * i) % pitch);
+        const float4 v = m[i];
+        const float4 e = eta ? eta[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float mv[4] = {v.x, v.y, v.z, v.w}, ev[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (x + c < nx) bad |= !(mv[c] > 0.0f) || !isfinite(mv[c]) || !(ev[c] >= 0.0f) || !isfinite(ev[c]);
     }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
 }
 
 cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag,
                                   cudaStream_t s) {
-    int64_t rows = (int64_t)g.nz * g.ny;
-    int blocks = (int)(rows < 148 * 8 ? rows : 148 * 8);
+    const int64_t n4 = (int64_t)g.nz * g.plane / 4;
+    int blocks = (int)((n4 + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    validate_kernel<<<blocks, 128, 0, s>>>(m, eta, g.nz, g.ny, g.nx, g.pitch, flag);
+    validate_kernel<<<blocks, 256, 0, s>>>((const float4*)m, (const float4*)eta, n4, g.nx, g.pitch, flag);
     return cudaGetLastError();
 }
 
@@ -224,11 +235,13 @@ cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s) {
 // NaN/Inf check of the owned wavefield and of trace rows [t0, t1).
 __global__ void check_finite_kernel(Geom g, const float* __restrict__ u, const float* __restrict__ traces,
                                     int64_t t0, int64_t t1, int nr, unsigned* flag) {
-    int64_t rows = (int64_t)g.nz * g.ny;
+    // owned planes incl. the (always zero) pitch padding: a flat float4 walk
+    const float4* u4 = reinterpret_cast<const float4*>(u + (int64_t)g.R * g.plane);
+    const int64_t n4 = (int64_t)g.nz * g.plane / 4;
     bool bad = false;
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const float* ur = u + (int64_t)g.R * g.plane + r * g.pitch;
-        for (int x = threadIdx.x; x < g.nx; x += blockDim.x) bad |= !isfinite(ur[x]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = u4[i];
+        bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
     }
     if (traces) {
         int64_t tot = (t1 - t0) * nr;
@@ -240,7 +253,7 @@ __global__ void check_finite_kernel(Geom g, const float* __restrict__ u, const f
 
 cudaError_t launch_check_finite(const Geom& g, const float* u, const float* traces, int64_t t0, int64_t t1,
                                 int nr, unsigned* flag, cudaStream_t s) {
-    check_finite_kernel<<<148 * 4, 256, 0, s>>>(g, u, traces, t0, t1, nr, flag);
+    check_finite_kernel<<<148 * 8, 256, 0, s>>>(g, u, traces, t0, t1, nr, flag);
     return cudaGetLastError();
 }
 

@@ -420,6 +420,8 @@ struct StreamPlan {
     int nthreads = 0;
     int TX = 0, TY = 0;
     int nzc = 1, zc = 0;
+    unsigned long long* d_count = nullptr;  // tile-planes with a != 1 (inside the flags allocation)
+    int64_t nflags = 0;
 };
 
 namespace {
@@ -555,13 +557,13 @@ int variant() {
     }
 
 cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* b, const float* a,
-                           StreamPlan** plan, int* eta_tiles_pct, cudaStream_t s) {
+                           StreamPlan** plan, cudaStream_t s) {
     *plan = nullptr;
     if (g.ndim != 3) return cudaErrorNotSupported;
     StreamPlan* p = new StreamPlan();
     p->R = g.R;
     cudaError_t e = cudaSuccess;
-    AW_STREAM_DISPATCH(g.R, e = setup<C>(p, g); if (e == cudaSuccess) e = make_maps<C>(p, g, ubuf, b, a));
+    AW_STREAM_DISPATCH(g.R, e = setup<C>(p, g));
     if (e != cudaSuccess) {
         delete p;
         return e;
@@ -576,37 +578,44 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     p->zc = (g.nz + nzc - 1) / nzc;
     p->nzc = (g.nz + p->zc - 1) / p->zc;
     const int64_t nflags = (int64_t)ntiles * g.nz;
-    e = cudaMalloc(&p->flags, nflags);
-    if (e != cudaSuccess) {
+    if ((e = cudaMalloc(&p->flags, nflags + sizeof(unsigned long long) + 16)) != cudaSuccess) {
         delete p;
         return e;
     }
-    if (a) {
-        dim3 grid(ntiles, g.nz);
-        eta_flags_kernel<<<grid, 256, 0, s>>>(g, a, p->TX, p->TY, p->ntx, p->nty, p->flags);
-        unsigned long long* cnt = nullptr;
-        e = cudaMallocAsync(&cnt, sizeof(unsigned long long), s);
-        if (e == cudaSuccess) {
-            cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s);
-            count_flags_kernel<<<148, 256, 0, s>>>(p->flags, nflags, cnt);
-            unsigned long long h = 0;
-            cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            cudaFreeAsync(cnt, s);
-            *eta_tiles_pct = (int)(100.0 * (double)h / (double)nflags + 0.5);
-        }
-    } else {
-        cudaMemsetAsync(p->flags, 0, nflags, s);
-        *eta_tiles_pct = 0;
-    }
-    e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFree(p->flags);
-        delete p;
+    p->d_count = reinterpret_cast<unsigned long long*>(p->flags + (nflags + 15) / 16 * 16 - 0);
+    if ((e = stream_refresh(p, g, ubuf, b, a, s)) != cudaSuccess) {
+        stream_release(p);
         return e;
     }
     *plan = p;
     return cudaSuccess;
+}
+
+// (Re)encode the tensor maps and recompute the per-(plane, tile) eta flags; no host sync.
+cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a,
+                           cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    AW_STREAM_DISPATCH(p->R, e = make_maps<C>(p, g, ubuf, b, a));
+    if (e != cudaSuccess) return e;
+    const int ntiles = p->ntx * p->nty;
+    const int64_t nflags = (int64_t)ntiles * g.nz;
+    cudaMemsetAsync(p->d_count, 0, sizeof(unsigned long long), s);
+    if (a) {
+        dim3 grid(ntiles, g.nz);
+        eta_flags_kernel<<<grid, 256, 0, s>>>(g, a, p->TX, p->TY, p->ntx, p->nty, p->flags);
+        count_flags_kernel<<<148, 256, 0, s>>>(p->flags, nflags, p->d_count);
+    } else {
+        cudaMemsetAsync(p->flags, 0, nflags, s);
+    }
+    p->nflags = nflags;
+    return cudaGetLastError();
+}
+
+// Percentage of (plane, tile) pairs that stream `a` (call after the stream synchronised).
+int stream_eta_tiles_pct(const StreamPlan* p) {
+    unsigned long long h = 0;
+    if (!p || cudaMemcpy(&h, p->d_count, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return p->nflags ? (int)(100.0 * (double)h / (double)p->nflags + 0.5) : 0;
 }
 
 void stream_release(StreamPlan* p) {
