@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -131,6 +132,8 @@ struct aw_grid {
     std::vector<int64_t> src_corner_lin;  // [ns][nc]
     std::vector<double> src_w64;          // [ns][nc]
     std::vector<int> ent_src, ent_beta;   // owned entries in CSR order
+    std::vector<int64_t> h_inj_lin;       // owned unique injection corners (CSR order)
+    std::vector<int> h_inj_ptr;           // their CSR ranges
     float* d_wavelet = nullptr;
     int64_t* d_inj_off = nullptr;
     int* d_inj_plane = nullptr;
@@ -318,6 +321,8 @@ void free_sources(aw_grid* g) {  // the device arrays are views into g->src_aren
     g->src_w64.clear();
     g->ent_src.clear();
     g->ent_beta.clear();
+    g->h_inj_lin.clear();
+    g->h_inj_ptr.clear();
 }
 void free_receivers(aw_grid* g) {  // views into g->rec_arena
     g->d_rec_id = nullptr;
@@ -417,6 +422,9 @@ aw_status prepare(aw_grid* g, double dt) {
         // refresh the maps and the eta flags (no allocation, no host synchronisation)
         cudaError_t e = g->plan ? aw::stream_refresh(g->plan, g->geom, ub, g->b, a, g->s)
                                 : aw::stream_prepare(g->geom, ub, g->b, a, &g->plan, g->s);
+        if (e == cudaSuccess)
+            e = aw::stream_set_injection(g->plan, g->geom, g->z0, g->h_inj_lin.data(), g->h_inj_ptr.data(), g->nuc,
+                                         g->s);
         if (e == cudaSuccess) {
             g->kernel_used = AW_KERNEL_STREAM;
             g->launch_count += a ? 2 : 0;
@@ -448,16 +456,21 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0
         ++*launches;
     }
     if (e0) CK(cudaEventRecord(e0, g->s));
+    // receivers + injection inside the stencil kernel (AW_NO_FUSE=1: separate sparse kernel, for A/B runs)
+    static const bool no_fuse = getenv("AW_NO_FUSE") != nullptr;
+    const bool fused = g->kernel_used == AW_KERNEL_STREAM && !no_fuse;
     if (g->kernel_used == AW_KERNEL_STREAM) {
+        aw::Sparse sp = sparse_view(g);
+        if (!fused) sp.nrl = sp.nuc = 0;
         CK(aw::launch_stencil_stream(g->plan, g->geom, g->coefs, cur, g->ubuf[cur], g->ubuf[nxt], g->b,
-                                     g->have_damp ? g->a : nullptr, g->halo, nxt, g->s));
+                                     g->have_damp ? g->a : nullptr, g->halo, nxt, sp, g->d_base, i, g->s));
     } else {
         CK(aw::launch_stencil_v1(g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->b, g->have_damp ? g->a : nullptr,
                                  g->halo, nxt, g->s));
     }
     ++*launches;
     if (e1) CK(cudaEventRecord(e1, g->s));
-    if (g->nrl + g->nuc > 0) {
+    if (!fused && g->nrl + g->nuc > 0) {
         CK(aw::launch_sparse_step(g->geom, sparse_view(g), g->ubuf[cur], g->ubuf[nxt], g->d_base, i, g->halo, nxt,
                                   g->s));
         ++*launches;
@@ -570,7 +583,7 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
             aw_status st = get_graph(g, G, g->cur, &exec);
             if (st) return st;
             CK(cudaGraphLaunch(exec, g->s));
-            *launches += (int64_t)G * (1 + (g->nrl + g->nuc > 0 ? 1 : 0)) + 1;
+            *launches += (int64_t)G * (1 + (g->kernel_used != AW_KERNEL_STREAM && g->nrl + g->nuc > 0 ? 1 : 0)) + 1;
             done += G;
             if (G & 1) g->cur = 1 - g->cur;
         }
@@ -885,6 +898,7 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
             inj_off.push_back(uoff);
             inj_plane.push_back((int)zl);
             inj_ptr.push_back((int)e);
+            g->h_inj_lin.push_back(ents[e].lin);
         }
         int64_t zl, uoff, moff;
         lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
@@ -895,6 +909,7 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
         g->ent_beta.push_back(ents[e].beta);
     }
     inj_ptr.push_back((int)ents.size());
+    g->h_inj_ptr = inj_ptr;
     g->nuc = (int)inj_off.size();
     g->nent = (int)ents.size();
     Packer pk;

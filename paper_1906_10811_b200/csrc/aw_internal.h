@@ -91,6 +91,9 @@ int stream_eta_tiles_pct(const StreamPlan* p);
 void stream_release(StreamPlan* p);
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
                                   const float* ucur, float* unext, const float* b, const float* a,
-                                  const Halo& halo, int parity_next, cudaStream_t s);
+                                  const Halo& halo, int parity_next, const Sparse& sp, const int64_t* d_base,
+                                  int step_i, cudaStream_t s);
+cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const int64_t* corner_lin, const int* ptr,
+                                 int nuc, cudaStream_t s);
 
 }  // namespace aw

@@ -36,8 +36,11 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
+#include <vector>
 
 #include "aw_internal.h"
 
@@ -107,7 +110,7 @@ struct Cfg {
     static constexpr int SP = DP + 1;     // (u^{n-1}, b, a) ring of the output planes
     static constexpr int NWARPS_COMP = TY / RY;
     static constexpr int NCOMP = 32 * NWARPS_COMP;
-    static constexpr int NTHREADS = NCOMP + 64;  // + producer warps for the u^n ring and the streams ring
+    static constexpr int NTHREADS = NCOMP + 96;  // + u^n producer, streams producer, receivers warp
     static constexpr int STAGE_FLOATS = TXP * TYP;
     static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;                 // TMA transaction bytes
     static constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;  // 128-B aligned ring slots
@@ -117,8 +120,8 @@ struct Cfg {
     static constexpr int PSTAGE_FLOATS = 3 * PTILE_FLOATS;  // u^{n-1}, b, a
     static constexpr size_t U_BYTES = (size_t)SU * STAGE_STRIDE;
     static constexpr size_t P_BYTES = (size_t)SP * PSTAGE_FLOATS * 4;
-    // + full/empty barriers of both rings + one "stage carries a" word per streams stage
-    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + SP * sizeof(int);
+    // + full/empty barriers of both rings + 3 metadata words per streams stage
+    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + 3 * SP * sizeof(int);
     static_assert(TY % RY == 0, "tile shape");
     static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
 };
@@ -128,7 +131,7 @@ struct StreamArgs {
     Coefs c;
     float* unext;            // buffer base (plane -R)
     const float* a;          // may be null (no damping)
-    const uint8_t* flags;    // [nz][ntiles]: 1 if any a != 1 in the tile-plane
+    const uint8_t* flags;    // [ntiles][nz]: 1 if any a != 1 in the tile-plane
     float* lo;               // team halo targets (null if none)
     int64_t lo_off;
     float* hi;
@@ -136,6 +139,21 @@ struct StreamArgs {
     int ntx, nty;            // tiles along x, y
     int nzc, zc;             // z chunks and planes per chunk
     int nitems;              // ntiles * nzc
+    // fused per-step sparse work (SURVEY §8(a) a7 injection, a8 receivers)
+    const int2* tpsc;        // [ntiles][nz]: {first entry, count} of injection corners in the tile-plane
+    const int4* tpe;         // entries: {tile-local point ly*64+lx, csr begin, csr end, 0}
+    const int* inj_src;      // [nent] source index (CSR: corner ascending, then source)
+    const float* inj_s;      // [nent] fp32 scale dt^2 w / (m + eta dt/2)
+    const float* wavelet;    // [nt_max][ns]
+    int ns;
+    int nrl, nr, nc;         // owned receivers, trace row length, corners per point
+    const int* rec_id;
+    const int64_t* rec_off;  // element offsets into the u^n buffer (-1: skipped corner)
+    const float* rec_w;
+    float* traces;           // [nt_max][nr]
+    const float* ucur;       // u^n buffer base (plane -R)
+    const int64_t* d_base;   // the step index is n = *d_base + step_i (graph-replay friendly)
+    int step_i;
 };
 
 struct StreamMaps {
@@ -162,9 +180,9 @@ struct Ring {
 template <class C, bool INTERIOR, bool TEAM>
 __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* ring, const float* pring,
                                              uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
-                                             const volatile int* pflag,
+                                             const volatile int* pmeta,
                                              int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
-                                             Ring& rp) {
+                                             Ring& rp, int64_t step_n) {
     constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
     const Geom& g = A.g;
     const int nz = g.nz;
@@ -208,7 +226,9 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                 // (u^{n-1}, b, a) tiles of the output plane
                 mbar_wait(&fullP[rp.slot], rp.phase);
                 const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + lane;
-                const bool use_a = pflag[rp.slot] != 0;  // set by the streams producer before its arrive
+                // stage metadata written by the streams producer before its arrive: use_a, injection list
+                const bool use_a = pmeta[3 * rp.slot] != 0;
+                const int inj_first = pmeta[3 * rp.slot + 1], inj_count = pmeta[3 * rp.slot + 2];
                 // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
                 float2 col[RY + 2 * R];
 #pragma unroll
@@ -238,15 +258,31 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                     const float2 t = fma2(two, uc, f2(-um.x, -um.y));
                     const float2 wv = fma2(bb, L, t);
                     const float2 rr = mul2(add2(one, f2(-aa.x, -aa.y)), um);
-                    const float2 un = fma2(aa, wv, rr);
-                    float* o = outp + i * pitch;
-                    if (ok_a[i]) o[0] = un.x;
-                    if (ok_b[i]) o[32] = un.y;
-                    res[i] = un;
+                    res[i] = fma2(aa, wv, rr);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&emptyP[rp.slot]);
                 rp.advance(SP);
+                // fused injection: u^{n+1}[c] = fma(s, q[n][src], u^{n+1}[c]) over the
+                // corner's sources in CSR order, applied by the thread that owns the corner, before storing
+                for (int e = inj_first; e < inj_first + inj_count; ++e) {
+                    const int4 en = A.tpe[e];
+                    const int yl = en.x >> 6, xl = en.x & 63;
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) {
+                        if (yl != ly + i || (xl & 31) != lane) continue;
+                        float v = xl < 32 ? res[i].x : res[i].y;
+                        const float* qn = A.wavelet + step_n * A.ns;
+                        for (int k = en.y; k < en.z; ++k) v = __fmaf_rn(A.inj_s[k], qn[A.inj_src[k]], v);
+                        if (xl < 32) res[i].x = v; else res[i].y = v;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < RY; ++i) {
+                    float* o = outp + i * pitch;
+                    if (ok_a[i]) o[0] = res[i].x;
+                    if (ok_b[i]) o[32] = res[i].y;
+                }
                 if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
                     // fused exchange: boundary planes also go straight into the neighbour's halo
                     const int64_t om = (outp - A.unext) - (int64_t)R * plane;  // model-layout index
@@ -288,7 +324,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     uint64_t* emptyU = fullU + SU;
     uint64_t* fullP = emptyU + SU;
     uint64_t* emptyP = fullP + SP;
-    int* pflag = reinterpret_cast<int*>(emptyP + SP);
+    int* pmeta = reinterpret_cast<int*>(emptyP + SP);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -310,6 +346,20 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const int nz = g.nz;
     const int ntiles = A.ntx * A.nty;
 
+    const int64_t step_n = *A.d_base + A.step_i;
+    if (warp == C::NWARPS_COMP + 2) {
+        // ---------------- receivers warp: rec[n][r] = fma chain of u^n corners --------
+        for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
+            float acc = 0.0f;
+            for (int beta = 0; beta < A.nc; ++beta) {
+                const int64_t off = A.rec_off[(int64_t)r * A.nc + beta];
+                if (off < 0) continue;
+                acc = __fmaf_rn(A.rec_w[(int64_t)r * A.nc + beta], A.ucur[off], acc);
+            }
+            A.traces[step_n * A.nr + A.rec_id[r]] = acc;
+        }
+        return;
+    }
     if (warp >= C::NWARPS_COMP) {
         // ---------------- producer warps ----------------
         // warp NWARPS_COMP: u^n plane tiles (with halo) into the ring, D planes ahead, and L2
@@ -345,15 +395,18 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         if (z >= ze) return;
                         tma_prefetch_l2_3d(&M.un, x0, y0, z + R);
                         tma_prefetch_l2_3d(&M.b, x0, y0, z);
-                        if (A.a && A.flags[(int64_t)z * ntiles + tile]) tma_prefetch_l2_3d(&M.a, x0, y0, z);
+                        if (A.a && A.flags[(int64_t)tile * nz + z]) tma_prefetch_l2_3d(&M.a, x0, y0, z);
                     };
                     for (int z = zb; z < zb + PD; ++z) l2_prefetch(z);
                     for (int z = zb; z < ze; ++z) {
                         l2_prefetch(z + PD);
-                        const bool use_a = A.a && A.flags[(int64_t)z * ntiles + tile];
+                        const bool use_a = A.a && A.flags[(int64_t)tile * nz + z];  // [tile][z]: L1-friendly
+                        const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
                         float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
                         mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
-                        pflag[rr.slot] = use_a;  // published by the release of the arrive below
+                        pmeta[3 * rr.slot] = use_a;  // published by the release of the arrive below
+                        pmeta[3 * rr.slot + 1] = tp.x;
+                        pmeta[3 * rr.slot + 2] = tp.y;
                         mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
                         tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
                         tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
@@ -375,16 +428,16 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         const int ze = min(nz, zb + A.zc);
         const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
         if (x0 + TX <= g.nx && y0 + TY <= g.ny)
-            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pflag, tile, zb, ze, x0, y0, lane, ly,
-                                        ru, rp);
+            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane, ly,
+                                        ru, rp, step_n);
         else
-            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pflag, tile, zb, ze, x0, y0, lane,
-                                         ly, ru, rp);
+            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane,
+                                         ly, ru, rp, step_n);
     }
 }
 
 // ---------------------------------------------------------------------------
-// eta flags: flags[z][tile] = 1 iff some a != 1 in the tile-plane
+// eta flags: flags[tile][z] = 1 iff some a != 1 in the tile-plane
 // ---------------------------------------------------------------------------
 __global__ void eta_flags_kernel(Geom g, const float* __restrict__ a, int TX, int TY, int ntx, int nty,
                                  uint8_t* flags) {
@@ -397,7 +450,7 @@ __global__ void eta_flags_kernel(Geom g, const float* __restrict__ a, int TX, in
         if (x < g.nx && y < g.ny) any |= a[(int64_t)z * g.plane + (int64_t)y * g.pitch + x] != 1.0f;
     }
     any = __syncthreads_or(any);
-    if (threadIdx.x == 0) flags[(int64_t)z * ntx * nty + tile] = any ? 1 : 0;
+    if (threadIdx.x == 0) flags[(int64_t)tile * g.nz + z] = any ? 1 : 0;
 }
 
 __global__ void count_flags_kernel(const uint8_t* flags, int64_t n, unsigned long long* cnt) {
@@ -422,6 +475,9 @@ struct StreamPlan {
     int nzc = 1, zc = 0;
     unsigned long long* d_count = nullptr;  // tile-planes with a != 1 (inside the flags allocation)
     int64_t nflags = 0;
+    int2* tpsc = nullptr;                   // [ntiles][nz] injection lists (fused sparse work)
+    int4* tpe = nullptr;
+    size_t tpe_cap = 0;
 };
 
 namespace {
@@ -492,9 +548,11 @@ cudaError_t make_maps(StreamPlan* p, const Geom& g, const float* const* ubuf, co
 }
 
 template <class C>
-cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, float* unext, const float* b,
-                   const float* a, const Halo& halo, int parity_next, cudaStream_t s) {
+cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur, float* unext,
+                   const float* b, const float* a, const Halo& halo, int parity_next, const Sparse& sp,
+                   const int64_t* d_base, int step_i, cudaStream_t s) {
     StreamArgs A;
+    std::memset(&A, 0, sizeof A);
     A.g = g;
     A.c = c;
     A.unext = unext;
@@ -509,6 +567,22 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.nzc = p->nzc;
     A.zc = p->zc;
     A.nitems = p->ntx * p->nty * p->nzc;
+    A.tpsc = sp.nuc > 0 ? p->tpsc : nullptr;
+    A.tpe = p->tpe;
+    A.inj_src = sp.inj_src;
+    A.inj_s = sp.inj_s;
+    A.wavelet = sp.wavelet;
+    A.ns = sp.ns;
+    A.nrl = sp.nrl;
+    A.nr = sp.nr;
+    A.nc = sp.nc;
+    A.rec_id = sp.rec_id;
+    A.rec_off = sp.rec_off;
+    A.rec_w = sp.rec_w;
+    A.traces = sp.traces;
+    A.ucur = ucur;
+    A.d_base = d_base;
+    A.step_i = step_i;
     if (A.lo || A.hi)
         stream_kernel<C, true><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
     else
@@ -621,15 +695,62 @@ int stream_eta_tiles_pct(const StreamPlan* p) {
 void stream_release(StreamPlan* p) {
     if (!p) return;
     if (p->flags) cudaFree(p->flags);
+    if (p->tpsc) cudaFree(p->tpsc);
+    if (p->tpe) cudaFree(p->tpe);
     delete p;
+}
+
+// Injection lists per tile-plane for the fused kernel.  corner_lin: the owned unique injection
+// corners (global row-major index, ascending), ptr: their CSR ranges into the entry arrays.
+cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const int64_t* corner_lin, const int* ptr,
+                                 int nuc, cudaStream_t s) {
+    const int ntiles = p->ntx * p->nty;
+    const int64_t ntp = (int64_t)ntiles * g.nz;
+    cudaError_t e;
+    if (!p->tpsc && (e = cudaMalloc(&p->tpsc, ntp * sizeof(int2))) != cudaSuccess) return e;
+    std::vector<std::pair<int64_t, int4>> ents;  // key = tile*nz + z
+    const int64_t per_plane = (int64_t)g.ny * g.nx;
+    for (int c = 0; c < nuc; ++c) {
+        const int64_t lin = corner_lin[c];
+        const int z = (int)(lin / per_plane - z0);
+        const int y = (int)((lin % per_plane) / g.nx), x = (int)(lin % g.nx);
+        const int tile = (y / p->TY) * p->ntx + x / p->TX;
+        const int pos = (y % p->TY) * 64 + (x % p->TX);
+        ents.push_back({(int64_t)tile * g.nz + z, make_int4(pos, ptr[c], ptr[c + 1], 0)});
+    }
+    std::stable_sort(ents.begin(), ents.end(),
+                     [](const std::pair<int64_t, int4>& a, const std::pair<int64_t, int4>& b) { return a.first < b.first; });
+    std::vector<int2> tpsc_h;  // only the touched keys are uploaded; the rest is zero (count 0)
+    if ((e = cudaMemsetAsync(p->tpsc, 0, ntp * sizeof(int2), s)) != cudaSuccess) return e;
+    if (ents.empty()) return cudaSuccess;
+    if (p->tpe_cap < ents.size()) {
+        if (p->tpe) cudaFree(p->tpe);
+        p->tpe = nullptr;
+        p->tpe_cap = 0;
+        if ((e = cudaMalloc(&p->tpe, ents.size() * sizeof(int4))) != cudaSuccess) return e;
+        p->tpe_cap = ents.size();
+    }
+    std::vector<int4> tpe_h(ents.size());
+    for (size_t i = 0; i < ents.size(); ++i) tpe_h[i] = ents[i].second;
+    if ((e = cudaMemcpyAsync(p->tpe, tpe_h.data(), tpe_h.size() * sizeof(int4), cudaMemcpyHostToDevice, s)))
+        return e;
+    for (size_t i = 0; i < ents.size();) {
+        size_t j = i;
+        while (j < ents.size() && ents[j].first == ents[i].first) ++j;
+        const int2 v = make_int2((int)i, (int)(j - i));
+        if ((e = cudaMemcpyAsync(p->tpsc + ents[i].first, &v, sizeof v, cudaMemcpyHostToDevice, s))) return e;
+        i = j;
+    }
+    return cudaStreamSynchronize(s);  // the host staging vectors die here
 }
 
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur,
                                   float* unext, const float* b, const float* a, const Halo& halo, int parity_next,
-                                  cudaStream_t s) {
-    (void)ucur;  // read through the tensor map of buffer parity_cur
+                                  const Sparse& sp, const int64_t* d_base, int step_i, cudaStream_t s) {
+    // u^n is read through the tensor map of buffer parity_cur (stencil) and ucur (receivers)
     if (!p) return cudaErrorNotSupported;
-    AW_STREAM_DISPATCH(p->R, return launch<C>(p, g, c, parity_cur, unext, b, a, halo, parity_next, s));
+    AW_STREAM_DISPATCH(p->R, return launch<C>(p, g, c, parity_cur, ucur, unext, b, a, halo, parity_next, sp, d_base,
+                                              step_i, s));
     return cudaErrorNotSupported;
 }
 
