@@ -177,3 +177,21 @@ def run(mode, shape, extent, space_order, m, dt, nt, *, damp=None, origin=None,
                             int(n0), int(nt), ns, _p(sc), _p(wv), nr, _p(rc), _p(rec) if nr else None,
                             _p(uc), _p(up), int(nthreads)), "run")
     return uc, up, rec
+
+
+def diffusion_run(mode, shape, extent, space_order, nu, dt, nt, u0, nthreads=0):
+    """NEXT-2: forward-Euler diffusion; returns u^nt (fp32 for mode 0, else fp64)."""
+    L = lib()
+    if not hasattr(L, "_diff_sig"):
+        L.oracle_diffusion_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_int]
+        L._diff_sig = True
+    shape = tuple(int(s) for s in shape)
+    dtype = np.float32 if mode == FP32CANON else np.float64
+    sh = np.asarray(shape, dtype=np.int64)
+    ex = np.asarray(extent, dtype=np.float64)
+    u = np.array(u0, dtype=dtype, copy=True).reshape(shape)
+    _check(L.oracle_diffusion_run(mode, len(shape), _p(sh), _p(ex), space_order, float(nu), float(dt), int(nt),
+                                  _p(u), int(nthreads)), "diffusion_run")
+    return u

@@ -475,3 +475,97 @@ int oracle_source_scales(int ndim, const int64_t* shape, const double* extent, c
     free(w);
     return st;
 }
+
+/* ===========================================================================
+ * NEXT-2: the paper's own benchmark operator, 2D (or 3D) diffusion
+ *   u_t = nu (u_xx + u_yy)            PAPER.md:732-736 [Evaluation > Examined problem]
+ * discretised as in the paper's Devito listing: time_order=1
+ * (forward Euler, `solve(eqn, u.forward)`), FD shortcuts u.dx2 + u.dy2 of the
+ * given space order, zero padding.  The worked kernel
+ * folds nu into the weights (5.0e-1F = nu*1, -1.0F = nu*-2).
+ *
+ * ORACLE_FP32CANON sequence per point (this build's reading, DESIGN.md §3 Q22):
+ *   L = C0*u;  for d = ndim-1..0, j = 1..R: L = fmaf(C[d][j], u_{p-je_d} + u_{p+je_d}, L)
+ *   u_next = fmaf(D, L, u)             with D = fl32(nu*dt) (fp64 product, one rounding)
+ * ORACLE_FP64CANON: same sequence in fp64 with the same fp32 C, C0, D.
+ * ORACLE_FP64EXACT: u_next = u + nu*dt*sum_d sum_j c_|j|/h_d^2 u(p+j e_d) in fp64.
+ * u holds the initial field on entry and u^nt on return (float or double by mode).
+ * ------------------------------------------------------------------------- */
+int oracle_diffusion_run(int mode, int ndim, const int64_t* shape, const double* extent, int space_order,
+                         double nu, double dt, int nt, void* u, int nthreads) {
+    if (ndim < 2 || ndim > 3) return OR_EINVAL;
+    if (space_order < 2 || space_order > 2 * MAXR || (space_order & 1)) return OR_EINVAL;
+    if (mode < 0 || mode > 2 || nt < 0) return OR_EINVAL;
+    const int R = space_order / 2;
+    int64_t N = 1;
+    for (int d = 0; d < ndim; ++d) {
+        if (shape[d] < R + 1) return OR_EINVAL;
+        N *= shape[d];
+    }
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    float C[3 * (MAXR + 1)], C0;
+    double C64[3 * (MAXR + 1)], C064;
+    oracle_axis_coeffs(ndim, shape, extent, space_order, C, &C0, C64, &C064);
+    const float D = (float)(nu * dt);
+    const double D64 = nu * dt;
+    size_t esz = (mode == ORACLE_FP32CANON) ? sizeof(float) : sizeof(double);
+    void* nxt = malloc(esz * N);
+    void* cur = malloc(esz * N);
+    if (!nxt || !cur) { free(nxt); free(cur); return OR_ENOMEM; }
+    memcpy(cur, u, esz * N);
+    for (int step = 0; step < nt; ++step) {
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < N; ++p) {
+            int64_t idx[3], q[3];
+            int64_t rem = p;
+            for (int d = ndim - 1; d >= 0; --d) { idx[d] = rem % shape[d]; rem /= shape[d]; }
+            if (mode == ORACLE_FP32CANON) {
+                const float* uc = (const float*)cur;
+                float L = C0 * uc[p];
+                for (int d = ndim - 1; d >= 0; --d)
+                    for (int j = 1; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] - j;
+                        float lo = inside(ndim, shape, q) ? uc[lin_index(ndim, shape, q)] : 0.0f;
+                        q[d] = idx[d] + j;
+                        float hi = inside(ndim, shape, q) ? uc[lin_index(ndim, shape, q)] : 0.0f;
+                        float pair = lo + hi;
+                        L = fmaf(C[d * (MAXR + 1) + j], pair, L);
+                    }
+                ((float*)nxt)[p] = fmaf(D, L, uc[p]);
+            } else if (mode == ORACLE_FP64CANON) {
+                const double* uc = (const double*)cur;
+                double L = (double)C0 * uc[p];
+                for (int d = ndim - 1; d >= 0; --d)
+                    for (int j = 1; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] - j;
+                        double lo = inside(ndim, shape, q) ? uc[lin_index(ndim, shape, q)] : 0.0;
+                        q[d] = idx[d] + j;
+                        double hi = inside(ndim, shape, q) ? uc[lin_index(ndim, shape, q)] : 0.0;
+                        L = fma((double)C[d * (MAXR + 1) + j], lo + hi, L);
+                    }
+                ((double*)nxt)[p] = fma((double)D, L, uc[p]);
+            } else {
+                const double* uc = (const double*)cur;
+                double L = 0.0;
+                for (int d = 0; d < ndim; ++d)
+                    for (int j = -R; j <= R; ++j) {
+                        memcpy(q, idx, sizeof(q));
+                        q[d] = idx[d] + j;
+                        double v = inside(ndim, shape, q) ? uc[lin_index(ndim, shape, q)] : 0.0;
+                        L += C64[d * (MAXR + 1) + (j < 0 ? -j : j)] * v;
+                    }
+                ((double*)nxt)[p] = uc[p] + D64 * L;
+            }
+        }
+        void* t = cur; cur = nxt; nxt = t;  /* rotation t_k = (time+k) mod 2 */
+    }
+    memcpy(u, cur, esz * N);
+    free(cur); free(nxt);
+    return OR_OK;
+}

@@ -601,8 +601,8 @@ using C6 = Cfg<6, 32, 4, 2, 3, 0, 1>;
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
 using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
-using C4v1 = Cfg<4, 32, 4, 4, 3, 0, 1>;
-using C4v2 = Cfg<4, 32, 4, 2, 2, 6, 1>;  // round-1 v4 (L2 prefetch 6 planes ahead)
+using C4v1 = Cfg<4, 32, 4, 3, 4, 0, 1>;
+using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
 using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
 
 int variant() {
