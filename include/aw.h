@@ -226,6 +226,30 @@ aw_status aw_team_connect_local(aw_grid** grids, int world);
 /* Drive virtual ranks step by step on their streams (one process). */
 aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt);
 
+/* ------------------------------------------------------------------------
+ * NEXT-2: the paper's own benchmark operator (PAPER.md:732-748 [Evaluation >
+ * Examined problem]): 2D diffusion  u_t = nu (u_xx + u_yy), forward Euler
+ * (time_order 1, solve(eqn, u.forward)), space order 2..16, zero padding.
+ * Per point (fp32, DESIGN.md §3 Q22):  L = C0 u; pairs fastest axis first;
+ * u_next = fma(fl32(nu*dt), L, u).  Same conventions as the acoustic calls:
+ * [H|D] arrays, C-order (n0, n1), h_d = extent_d/(n_d-1), synchronous calls.
+ * ------------------------------------------------------------------------ */
+typedef struct aw_diffusion aw_diffusion;
+
+/* ndim must be 2 (3 -> AW_EUNSUPPORTED); nu > 0; stream as in aw_dist (NULL = own). */
+aw_status aw_diffusion_create(aw_diffusion** out, int ndim, const int64_t* shape, const double* extent,
+                              int space_order, double nu, void* stream);
+/* u^0, fp32 [H|D], dense (n0, n1); NULL = zeros.  Resets the step counter. */
+aw_status aw_diffusion_set(aw_diffusion* d, const float* u);
+/* advance nt >= 0 steps with time step dt (> 0; no stability check). */
+aw_status aw_diffusion_run(aw_diffusion* d, int nt, double dt);
+/* copy the current field into out [H|D] (n0, n1). */
+aw_status aw_diffusion_read(aw_diffusion* d, float* out);
+aw_status aw_diffusion_stats(const aw_diffusion* d, aw_run_stats* out);
+/* AW_OPT_TIMING and AW_OPT_GRAPH_STEPS as for aw_set_option. */
+aw_status aw_diffusion_set_option(aw_diffusion* d, int option, int64_t value);
+void aw_diffusion_destroy(aw_diffusion* d);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

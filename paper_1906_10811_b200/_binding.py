@@ -74,6 +74,14 @@ _SIGS = {
     "aw_team_connect": (_S, [_P, _P]),
     "aw_team_connect_local": (_S, [ctypes.POINTER(_P), _I]),
     "aw_team_run": (_S, [ctypes.POINTER(_P), _I, _I, _D]),
+    # NEXT-2: the paper's diffusion operator
+    "aw_diffusion_create": (_S, [ctypes.POINTER(_P), _I, _P, _P, _I, _D, _P]),
+    "aw_diffusion_set": (_S, [_P, _P]),
+    "aw_diffusion_run": (_S, [_P, _I, _D]),
+    "aw_diffusion_read": (_S, [_P, _P]),
+    "aw_diffusion_stats": (_S, [_P, ctypes.POINTER(aw_run_stats)]),
+    "aw_diffusion_set_option": (_S, [_P, _I, _I64]),
+    "aw_diffusion_destroy": (None, [_P]),
 }
 EXPORTED = tuple(_SIGS)
 

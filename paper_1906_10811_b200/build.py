@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaw.so")
-SOURCES = ["aw_api.cu", "aw_kernels.cu", "aw_stream.cu"]
+SOURCES = ["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu"]
 HEADERS = ["aw_internal.h", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -650,6 +650,9 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
 extern "C" {
 
 const char* aw_last_error(void) { return g_err.c_str(); }
+
+// internal (aw_internal.h): lets the other translation units set the thread-local error text
+aw_status aw_internal_fail(aw_status st, const char* msg) { return fail(st, "%s", msg); }
 int aw_abi_version(void) { return AW_ABI_VERSION; }
 
 double aw_critical_dt(int ndim, const double* spacing, int space_order, double vmax) {
