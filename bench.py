@@ -233,11 +233,20 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1906_10811_b200 import build as awbuild
-    if rank == 0 or world == 1:
-        awbuild.build()
+    # AW_BENCH_SAME_DEVICE=1 + AW_BENCH_BACKEND=gloo: all ranks on cuda:0 (tests the multi-rank path,
+    # cudaIpc team included, on one GPU; NCCL refuses two ranks on one device)
+    if os.environ.get("AW_BENCH_SAME_DEVICE"):
+        local = 0
+    backend = os.environ.get("AW_BENCH_BACKEND", "nccl")
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    if rank == 0:
+        awbuild.build()  # (re)build only if stale; the other ranks wait before loading the .so
+    if world > 1:
         dist.barrier()
     import paper_1906_10811_b200 as aw
 
@@ -267,6 +276,11 @@ def main():
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def allreduce_max(v):
+        t = torch.tensor([v], dtype=torch.float64, device=device if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     verbose = bool(os.environ.get("AW_BENCH_VERBOSE"))
 
@@ -320,9 +334,7 @@ def main():
     launches = g.stats()["launches_total"] - launches0
     st = g.stats()
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce_max(ms)
     total_pts = float(np.prod(shape)) * nt * args.steps
     value = total_pts / (ms * 1e-3) / 1e9
 
@@ -346,9 +358,7 @@ def main():
         barrier()
         ems = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = allreduce_max(ems)
         h2d = m_h.numel() * 4 + (d_h.numel() * 4 if d_h is not None else 0) + wav_h.numel() * 4 \
             + spec["src"].size * 8 + spec["rec"].size * 8
         e2e = {"value": round(total_pts / (ems * 1e-3) / 1e9, 3), "unit": "Gpts/s", "h2d_bytes_per_step": int(h2d),
