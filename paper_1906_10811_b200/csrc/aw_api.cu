@@ -743,6 +743,9 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
         s0 = s0 + c[0] / h2;
     }
     g->coefs.C0 = (float)s0;
+    // fault-injection test hook ("perturbing one weight"): proves the parity
+    // tests can fail.  Never set in production; tests/test_gpu_faults.py uses it in a subprocess.
+    if (getenv("AW_DEBUG_PERTURB")) g->coefs.C[0][1] = nextafterf(g->coefs.C[0][1], 0.0f);
 
     aw_status st = AW_OK;
     auto bad = [&](cudaError_t e, const char* what) {
