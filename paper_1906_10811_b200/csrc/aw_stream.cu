@@ -644,11 +644,15 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     }
     p->ntx = (g.nx + p->TX - 1) / p->TX;
     p->nty = (g.ny + p->TY - 1) / p->TY;
-    // z chunks: enough items that the cyclic hand-out balances to ~1-2% (>= 16 items per CTA
+    // z chunks: enough items that the cyclic hand-out balances to ~1-2% (>= 8 items per CTA
     // when possible), chunks no thinner than 4R planes (warm-up overhead 2R/zc)
     const int ntiles = p->ntx * p->nty;
     int nzc = 1;
-    while ((int64_t)ntiles * nzc < 16LL * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
+    while ((int64_t)ntiles * nzc < 8LL * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
+    if (const char* zc_env = getenv("AW_STREAM_ZC")) {  // development knob: planes per z chunk
+        const int zc = atoi(zc_env);
+        if (zc > 0) nzc = (g.nz + zc - 1) / zc;
+    }
     p->zc = (g.nz + nzc - 1) / nzc;
     p->nzc = (g.nz + p->zc - 1) / p->zc;
     const int64_t nflags = (int64_t)ntiles * g.nz;
