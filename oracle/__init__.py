@@ -179,6 +179,47 @@ def run(mode, shape, extent, space_order, m, dt, nt, *, damp=None, origin=None,
     return uc, up, rec
 
 
+def fwi_gradient(mode, shape, extent, space_order, m, dt, nt, d_obs, *, damp=None, origin=None,
+                 src_coords=None, wavelet=None, rec_coords=None, nthreads=0):
+    """NEXT-3: adjoint-state gradient of J = 1/2 sum (rec - d_obs)^2 w.r.t. m (see aw_oracle.c).
+
+    Returns (grad [shape], residual [nt][nr], J); fp32 arrays for mode 0, else fp64.
+    """
+    L = lib()
+    if not hasattr(L, "_fwi_sig"):
+        P = ctypes.c_void_p
+        L.oracle_fwi_gradient.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int, P, P, ctypes.c_double,
+                                          ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P, P, P, P,
+                                          ctypes.c_int]
+        L._fwi_sig = True
+    ndim = len(shape)
+    shape = tuple(int(s) for s in shape)
+    dtype = np.float32 if mode == FP32CANON else np.float64
+    sh = np.asarray(shape, dtype=np.int64)
+    ex = np.asarray(extent, dtype=np.float64)
+    org = None if origin is None else np.asarray(origin, dtype=np.float64)
+    m = np.ascontiguousarray(m, np.float32).reshape(shape)
+    d = None if damp is None else np.ascontiguousarray(damp, np.float32).reshape(shape)
+    if src_coords is None:
+        ns, sc, wv = 0, None, None
+    else:
+        sc = np.ascontiguousarray(src_coords, np.float64).reshape(-1, ndim)
+        ns = sc.shape[0]
+        wv = np.ascontiguousarray(wavelet, np.float32).reshape(-1, ns)
+        if wv.shape[0] < nt:
+            raise ValueError("wavelet shorter than nt")
+    rc = np.ascontiguousarray(rec_coords, np.float64).reshape(-1, ndim)
+    nr = rc.shape[0]
+    dobs = np.ascontiguousarray(d_obs, np.float32).reshape(nt, nr)
+    grad = np.zeros(shape, dtype)
+    res = np.zeros((nt, nr), dtype)
+    J = ctypes.c_double(0.0)
+    _check(L.oracle_fwi_gradient(mode, ndim, _p(sh), _p(ex), _p(org), space_order, _p(m), _p(d), float(dt),
+                                 int(nt), ns, _p(sc), _p(wv), nr, _p(rc), _p(dobs), _p(grad), _p(res),
+                                 ctypes.byref(J), int(nthreads)), "fwi_gradient")
+    return grad, res, J.value
+
+
 def diffusion_run(mode, shape, extent, space_order, nu, dt, nt, u0, nthreads=0):
     """NEXT-2: forward-Euler diffusion; returns u^nt (fp32 for mode 0, else fp64)."""
     L = lib()

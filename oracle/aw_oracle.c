@@ -245,11 +245,28 @@ static int inj_cmp(const void* x, const void* y) {
  *   nthreads            : OpenMP threads (<=0: runtime default)
  * Three logical time slots rotated as t_k = (n + k) mod 3.
  * ------------------------------------------------------------------------- */
+static int oracle_run_ex(int mode, int ndim, const int64_t* shape, const double* extent, const double* origin,
+                         int space_order, const float* m, const float* damp, double dt, int n0, int nt,
+                         int ns, const double* src_coords, const float* wavelet, const double* wavelet64,
+                         int nr, const double* rec_coords, void* rec_out,
+                         void* u_cur, void* u_prev, int nthreads);
+
 int oracle_run(int mode, int ndim, const int64_t* shape, const double* extent, const double* origin,
                int space_order, const float* m, const float* damp, double dt, int n0, int nt,
                int ns, const double* src_coords, const float* wavelet,
                int nr, const double* rec_coords, void* rec_out,
                void* u_cur, void* u_prev, int nthreads) {
+    return oracle_run_ex(mode, ndim, shape, extent, origin, space_order, m, damp, dt, n0, nt, ns, src_coords,
+                         wavelet, NULL, nr, rec_coords, rec_out, u_cur, u_prev, nthreads);
+}
+
+/* wavelet64 (may be NULL): fp64 amplitudes used instead of `wavelet` by the fp64 modes
+ * (the FWI adjoint injects an fp64 residual in mode FP64EXACT; NEXT-3 below). */
+static int oracle_run_ex(int mode, int ndim, const int64_t* shape, const double* extent, const double* origin,
+                         int space_order, const float* m, const float* damp, double dt, int n0, int nt,
+                         int ns, const double* src_coords, const float* wavelet, const double* wavelet64,
+                         int nr, const double* rec_coords, void* rec_out,
+                         void* u_cur, void* u_prev, int nthreads) {
     if (ndim < 2 || ndim > 3) return OR_EINVAL;
     if (space_order < 2 || space_order > 2 * MAXR || (space_order & 1)) return OR_EINVAL;
     if (mode < 0 || mode > 2 || nt < 0) return OR_EINVAL;
@@ -427,16 +444,17 @@ int oracle_run(int mode, int ndim, const int64_t* shape, const double* extent, c
         for (int e = 0; e < ninj; ++e) {
             int s = inj[e].src, beta = inj[e].beta;
             int64_t c = inj[e].key;
-            float q32 = wavelet[(int64_t)n * ns + s];
+            float q32 = wavelet ? wavelet[(int64_t)n * ns + s] : 0.0f;
+            double q64 = wavelet64 ? wavelet64[(int64_t)n * ns + s] : (double)q32;
             if (mode == ORACLE_FP32CANON) {
                 float* un = (float*)vnext;
                 un[c] = fmaf(s32[s * nc + beta], q32, un[c]);
             } else if (mode == ORACLE_FP64CANON) {
                 double* un = (double*)vnext;
-                un[c] = fma((double)s32[s * nc + beta], (double)q32, un[c]);
+                un[c] = fma((double)s32[s * nc + beta], q64, un[c]);
             } else {
                 double* un = (double*)vnext;
-                un[c] += s64[s * nc + beta] * (double)q32;
+                un[c] += s64[s * nc + beta] * q64;
             }
         }
         /* 6.4 rotate: implicit in the slot index (k+1)%3 */
@@ -568,4 +586,128 @@ int oracle_diffusion_run(int mode, int ndim, const int64_t* shape, const double*
     memcpy(u, cur, esz * N);
     free(cur); free(nxt);
     return OR_OK;
+}
+
+/* ===========================================================================
+ * NEXT-3: gradient of the least-squares data misfit by the
+ * adjoint-state method -- the "inversion problems" the project exists for
+ * (PAPER.md:4, :17, :69, :98 [Plan / Introduction], :248 [Background]).
+ * The paper defines no gradient; this build's readings are DESIGN.md §3
+ * Q23-Q26:
+ *   J(m) = 1/2 sum_{n=0}^{nt-1} sum_r (rec[n][r] - d_obs[n][r])^2
+ * for the forward run of oracle_run from zero initial conditions.
+ * Differentiating the textbook update (per point p, holding u^n, u^{n-1}):
+ *   (m + eta dt/2) u^{n+1} = dt^2 (L u^n + P_s^T q^n) + m (2u^n - u^{n-1}) + (eta dt/2) u^{n-1}
+ *   => du^{n+1}_p/dm_p = -(u^{n+1} - 2u^n + u^{n-1})_p / (m_p + eta_p dt/2),
+ * and scaling the Lagrange multipliers by dt^2/(m + eta dt/2) turns the
+ * adjoint recursion into the SAME damped leapfrog run in reversed time with
+ * the residual injected at the receivers like a source:
+ *   psi^{-1} = psi^0 = 0,
+ *   psi^{k+1} = step(psi^k, psi^{k-1}) + inject(res[nt-1-k] at the receivers),
+ *   grad_p = -(1/dt^2) sum_{k=0}^{nt-1} psi^k_p D^n_p,   n = nt-1-k,
+ *   D^n = u^{n+1} - 2u^n + u^{n-1}           (u^{-1} = u^0 = 0).
+ * Pinned by central finite differences of J (tests/test_oracle_fwi_pins.py),
+ * which use only oracle_run -- none of the formulas above.
+ * Modes:
+ *   FP32CANON: res = fl32(rec - d_obs); D = fl32(fl32(u^{n+1} - 2u^n) + u^{n-1});
+ *              G = fmaf(psi^k, D, G) for k = 0..nt-1 from G = 0;
+ *              grad = fl32(-(double)G / (dt*dt))
+ *   FP64CANON: the same sequence in fp64 (propagations in fp64canon).
+ *   FP64EXACT: fp64 textbook propagations, res = rec - (double)d_obs,
+ *              grad = -sum_k psi^k D^n / dt^2.
+ * J = 0.5 * sum res^2 in fp64 (n-major, r-minor order).
+ * The whole forward history is kept (no checkpointing): plain and slow.
+ * grad_out, res_out: float (mode 0) or double; res_out may be NULL.
+ * ------------------------------------------------------------------------- */
+int oracle_fwi_gradient(int mode, int ndim, const int64_t* shape, const double* extent, const double* origin,
+                        int space_order, const float* m, const float* damp, double dt, int nt,
+                        int ns, const double* src_coords, const float* wavelet,
+                        int nr, const double* rec_coords, const float* d_obs,
+                        void* grad_out, void* res_out, double* J_out, int nthreads) {
+    if (ndim < 2 || ndim > 3 || mode < 0 || mode > 2 || nt < 1 || nr < 1 || !d_obs || !grad_out) return OR_EINVAL;
+    int64_t N = 1;
+    for (int d = 0; d < ndim; ++d) N *= shape[d];
+    const int f32 = mode == ORACLE_FP32CANON;
+    const size_t esz = f32 ? sizeof(float) : sizeof(double);
+    char* hist = (char*)calloc((size_t)(nt + 2) * N, esz); /* level l at slot l+1, l = -1..nt */
+    char* rec = (char*)calloc((size_t)nt * nr, esz);
+    char* res = (char*)calloc((size_t)nt * nr, esz);
+    char* wadj = (char*)calloc((size_t)nt * nr, esz);
+    char* ucur = (char*)calloc((size_t)N, esz);
+    char* uprev = (char*)calloc((size_t)N, esz);
+    char* G = (char*)calloc((size_t)N, esz);
+    int st = OR_OK;
+    double J = 0.0;
+    if (!hist || !rec || !res || !wadj || !ucur || !uprev || !G) { st = OR_ENOMEM; goto out; }
+#define LEVEL(l) (hist + (size_t)((l) + 1) * N * esz)
+
+    /* 1. forward run, one step per call, recording every level */
+    for (int n = 0; n < nt; ++n) {
+        memcpy(ucur, LEVEL(n), esz * N);
+        memcpy(uprev, LEVEL(n - 1), esz * N);
+        st = oracle_run_ex(mode, ndim, shape, extent, origin, space_order, m, damp, dt, n, 1, ns, src_coords,
+                           wavelet, NULL, nr, rec_coords, rec + (size_t)n * nr * esz, ucur, uprev, nthreads);
+        if (st) goto out;
+        memcpy(LEVEL(n + 1), ucur, esz * N);
+    }
+
+    /* 2. residual, misfit, time-reversed residual as the adjoint "wavelet" */
+    for (int n = 0; n < nt; ++n)
+        for (int r = 0; r < nr; ++r) {
+            size_t i = (size_t)n * nr + r, ir = (size_t)(nt - 1 - n) * nr + r;
+            if (f32) {
+                float v = ((float*)rec)[i] - d_obs[i];
+                ((float*)res)[i] = v;
+                ((float*)wadj)[ir] = v;
+                J += (double)v * (double)v;
+            } else {
+                double v = ((double*)rec)[i] - (double)d_obs[i];
+                ((double*)res)[i] = v;
+                ((double*)wadj)[ir] = v;
+                J += v * v;
+            }
+        }
+    J = 0.5 * J;
+
+    /* 3. adjoint run in reversed time with the imaging condition before each step */
+    memset(ucur, 0, esz * N);  /* psi^k     */
+    memset(uprev, 0, esz * N); /* psi^{k-1} */
+    for (int k = 0; k < nt; ++k) {
+        const int n = nt - 1 - k;
+        const char* u1 = LEVEL(n + 1);
+        const char* u0 = LEVEL(n);
+        const char* um1 = LEVEL(n - 1);
+        for (int64_t p = 0; p < N; ++p) {
+            if (f32) {
+                float D = (((const float*)u1)[p] - 2.0f * ((const float*)u0)[p]) + ((const float*)um1)[p];
+                ((float*)G)[p] = fmaf(((float*)ucur)[p], D, ((float*)G)[p]);
+            } else if (mode == ORACLE_FP64CANON) {
+                double D = (((const double*)u1)[p] - 2.0 * ((const double*)u0)[p]) + ((const double*)um1)[p];
+                ((double*)G)[p] = fma(((double*)ucur)[p], D, ((double*)G)[p]);
+            } else {
+                double D = ((const double*)u1)[p] - 2.0 * ((const double*)u0)[p] + ((const double*)um1)[p];
+                ((double*)G)[p] += ((double*)ucur)[p] * D;
+            }
+        }
+        if (k == nt - 1) break; /* psi^nt pairs with no forward level */
+        st = oracle_run_ex(mode, ndim, shape, extent, origin, space_order, m, damp, dt, k, 1, nr, rec_coords,
+                           f32 ? (const float*)wadj : NULL, f32 ? NULL : (const double*)wadj, 0, NULL, NULL,
+                           ucur, uprev, nthreads);
+        if (st) goto out;
+    }
+
+    /* 4. gradient = -G / dt^2 */
+    {
+        const double dt2 = dt * dt;
+        for (int64_t p = 0; p < N; ++p) {
+            if (f32) ((float*)grad_out)[p] = (float)(-(double)((float*)G)[p] / dt2);
+            else ((double*)grad_out)[p] = -((double*)G)[p] / dt2;
+        }
+    }
+    if (res_out) memcpy(res_out, res, esz * (size_t)nt * nr);
+    if (J_out) *J_out = J;
+#undef LEVEL
+out:
+    free(hist); free(rec); free(res); free(wadj); free(ucur); free(uprev); free(G);
+    return st;
 }
