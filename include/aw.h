@@ -73,7 +73,8 @@ enum {
     AW_OPT_KERNEL = 1,      /* value: AW_KERNEL_* */
     AW_OPT_TIMING = 2,      /* value 1: time every stencil launch with CUDA events (no graphs) */
     AW_OPT_GRAPH_STEPS = 3, /* value G >= 0: steps per captured CUDA graph (0 = no graphs) */
-    AW_OPT_CHECK_FINITE = 4 /* value 0/1 (default 1): aw_run checks traces + final field */
+    AW_OPT_CHECK_FINITE = 4, /* value 0/1 (default 1): aw_run checks traces + final field */
+    AW_OPT_CHECKPOINT_STEPS = 5 /* value K >= 0: aw_fwi_gradient segment length (0 = auto, see there) */
 };
 
 /* multi-rank description: one process (or virtual rank) per slab of axis 0 */
@@ -189,6 +190,8 @@ typedef struct {
     int kernel;           /* AW_KERNEL_* actually used */
     int eta_tiles;        /* percent of stream tiles that read `a` (damping present) */
     int64_t launches_total; /* kernels launched by this handle since creation (all calls) */
+    int64_t fwi_steps;    /* stencil steps of the last aw_fwi_gradient (forward + recompute + adjoint) */
+    int fwi_checkpoint;   /* checkpoint segment length K used by the last aw_fwi_gradient */
 } aw_run_stats;
 
 aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out);
@@ -225,6 +228,39 @@ aw_status aw_team_connect(aw_grid* g, const void* all_records);
 aw_status aw_team_connect_local(aw_grid** grids, int world);
 /* Drive virtual ranks step by step on their streams (one process). */
 aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt);
+
+/* ------------------------------------------------------------------------
+ * NEXT-3: gradient of the least-squares data misfit by the adjoint-state
+ * method -- the seismic inversion the project exists for (PAPER.md:4, :17,
+ * :69, :98, :248); the paper defines no gradient, the readings are DESIGN.md
+ * §3 Q23-Q26:
+ *   J(m) = 1/2 sum_{n<nt} sum_r (rec[n][r] - d_obs[n][r])^2
+ * for the forward run of nt steps from zero wavefields with the current
+ * sources and receivers.  Adjoint field psi = the same damped leapfrog run in
+ * reversed time with the time-reversed residual injected at the receivers
+ * (like sources: scale w dt^2/(m + eta dt/2), CSR by corner then receiver);
+ *   grad_p = -(1/dt^2) sum_{k<nt} psi^k_p (u^{n+1} - 2u^n + u^{n-1})_p,  n = nt-1-k,
+ * in the fp32 sequence of oracle_fwi_gradient (value-identical to it).
+ * The forward wavefield is replayed from checkpoints: segments of K steps,
+ * a history ring of K+2 levels plus the two levels at each later segment
+ * start (K + 2 + 2(ceil(nt/K) - 1) wavefield-sized device buffers, kept by the
+ * handle between calls); nt - K forward steps are recomputed.  K =
+ * AW_OPT_CHECKPOINT_STEPS, or (0) the largest K whose buffers fit in 60 % of
+ * the free device memory (K = nt: no recomputation).
+ *   d_obs     [nt][nr] fp32 [H|D] observed traces (row = step)
+ *   grad      fp32 [H|D] dJ/dm, dense grid layout (AW_GLOBAL/AW_LOCAL as aw_read_wavefield)
+ *   residual  [nt][nr] fp32 [H|D] rec - d_obs, or NULL
+ *   objective J (fp64 [H]), or NULL
+ * Starts from the reset state with time step dt (any dt); needs a model and
+ * receivers (AW_EINVAL without receivers), sources/traces covering nt steps.
+ * On return steps_done = nt and aw_read_receivers returns the forward traces;
+ * the wavefield levels hold adjoint data: aw_run / aw_read_wavefield return
+ * AW_ESTATE until aw_reset or aw_set_wavefield.  Single slab only (a team ->
+ * AW_EUNSUPPORTED).  AW_ENOMEM if even K = 1 does not fit; AW_ENONFINITE if J
+ * is not finite.
+ * ------------------------------------------------------------------------ */
+aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, float* grad, int layout,
+                          float* residual, double* objective);
 
 /* ------------------------------------------------------------------------
  * NEXT-2: the paper's own benchmark operator (PAPER.md:732-748 [Evaluation >

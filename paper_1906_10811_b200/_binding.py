@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 AW_OK, AW_EINVAL, AW_ENOMEM, AW_ECUDA, AW_ENCCL, AW_ESTATE, AW_EUNSUPPORTED, AW_ENONFINITE = 0, -1, -2, -3, -4, -5, -6, -7
 AW_GLOBAL, AW_LOCAL = 0, 1
 AW_KERNEL_AUTO, AW_KERNEL_V1, AW_KERNEL_STREAM = 0, 1, 2
-AW_OPT_KERNEL, AW_OPT_TIMING, AW_OPT_GRAPH_STEPS, AW_OPT_CHECK_FINITE = 1, 2, 3, 4
+AW_OPT_KERNEL, AW_OPT_TIMING, AW_OPT_GRAPH_STEPS, AW_OPT_CHECK_FINITE, AW_OPT_CHECKPOINT_STEPS = 1, 2, 3, 4, 5
 STATUS_NAMES = {0: "AW_OK", -1: "AW_EINVAL", -2: "AW_ENOMEM", -3: "AW_ECUDA", -4: "AW_ENCCL",
                 -5: "AW_ESTATE", -6: "AW_EUNSUPPORTED", -7: "AW_ENONFINITE"}
 
@@ -40,7 +40,8 @@ class aw_dist(ctypes.Structure):
 class aw_run_stats(ctypes.Structure):
     _fields_ = [("ms_total", ctypes.c_double), ("ms_stencil", ctypes.c_double), ("n_stencil", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("gpts", ctypes.c_double), ("points", ctypes.c_int64),
-                ("kernel", ctypes.c_int), ("eta_tiles", ctypes.c_int), ("launches_total", ctypes.c_int64)]
+                ("kernel", ctypes.c_int), ("eta_tiles", ctypes.c_int), ("launches_total", ctypes.c_int64),
+                ("fwi_steps", ctypes.c_int64), ("fwi_checkpoint", ctypes.c_int)]
 
 
 _P = ctypes.c_void_p
@@ -74,6 +75,8 @@ _SIGS = {
     "aw_team_connect": (_S, [_P, _P]),
     "aw_team_connect_local": (_S, [ctypes.POINTER(_P), _I]),
     "aw_team_run": (_S, [ctypes.POINTER(_P), _I, _I, _D]),
+    # NEXT-3: adjoint-state FWI gradient
+    "aw_fwi_gradient": (_S, [_P, _I, _D, _P, _P, _I, _P, ctypes.POINTER(_D)]),
     # NEXT-2: the paper's diffusion operator
     "aw_diffusion_create": (_S, [ctypes.POINTER(_P), _I, _P, _P, _I, _D, _P]),
     "aw_diffusion_set": (_S, [_P, _P]),
@@ -242,6 +245,18 @@ class Grid:
 
     def set_option(self, option, value):
         check(aw_set_option(self.handle, int(option), int(value)))
+
+    def fwi_gradient(self, nt, dt, d_obs, grad=None, residual=None, layout=AW_GLOBAL, want_residual=True):
+        """NEXT-3: (grad, residual, J) of J = 1/2 sum (rec - d_obs)^2 (include/aw.h aw_fwi_gradient)."""
+        keep = []
+        if grad is None:
+            grad = np.zeros(self.shape if layout == AW_GLOBAL else self.local_shape, np.float32)
+        if residual is None and want_residual:
+            residual = np.zeros((int(nt), self.nr), np.float32)
+        J = _D(0.0)
+        check(aw_fwi_gradient(self.handle, int(nt), float(dt), _ptr(d_obs, keep=keep), _ptr(grad), layout,
+                              _ptr(residual), ctypes.byref(J)))
+        return grad, residual, J.value
 
     # team plumbing
     def team_export(self) -> bytes:

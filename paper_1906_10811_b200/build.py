@@ -11,8 +11,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaw.so")
-SOURCES = ["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu"]
-HEADERS = ["aw_internal.h", os.path.join("..", "..", "include", "aw.h")]
+SOURCES = (["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu", "aw_fwi.cu"]
+           + [f"aw_stream_r{r}.cu" for r in range(1, 9)] + ["aw_stream_r4v.cu"])
+HEADERS = ["aw_internal.h", "aw_stream.cuh", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
@@ -30,16 +31,21 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    logs = []
+    # the translation units compile in parallel (aw_stream.cu dominates: one kernel per R and mode)
+    procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    objs, logs, errors = [], [], []
+    for src, obj, p in procs:
+        out, _ = p.communicate()
+        logs.append(out)
+        if p.returncode != 0:
+            errors.append(f"nvcc failed for {src}:\n{out}")
         objs.append(obj)
+    if errors:
+        raise RuntimeError("\n".join(errors))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)

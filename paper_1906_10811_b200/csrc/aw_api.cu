@@ -182,6 +182,28 @@ struct aw_grid {
     size_t src_cap = 0;
     char* rec_arena = nullptr;
     size_t rec_cap = 0;
+    // NEXT-3 FWI gradient: adjoint injection tables (receivers as sources), per-call buffers,
+    // the forward history ring + checkpoint pool (kept between calls)
+    std::vector<double> rec_w64;           // receivers' fp64 multilinear weights [nr][nc]
+    bool adj_valid = false;                // adjoint tables built for the current receivers
+    int adj_nuc = 0, adj_nent = 0;
+    std::vector<int64_t> h_adj_lin;
+    std::vector<int> h_adj_ptr;
+    char* adj_arena = nullptr;
+    size_t adj_cap = 0;
+    int64_t* d_adj_off = nullptr;
+    int* d_adj_plane = nullptr;
+    int* d_adj_ptr = nullptr;
+    int* d_adj_src = nullptr;
+    int64_t* d_adj_moff = nullptr;
+    double* d_adj_w64 = nullptr;
+    float* d_adj_s = nullptr;
+    char* fwi_arena = nullptr;             // d_obs, residual, adjoint wavelet, J, G
+    size_t fwi_cap = 0;
+    float* fwi_pool = nullptr;             // nbuf wavefield-sized buffers
+    int64_t fwi_pool_nbuf = 0;
+    int opt_ckpt = 0;                      // AW_OPT_CHECKPOINT_STEPS (0 = auto)
+    bool wave_invalid = false;             // after aw_fwi_gradient until aw_reset / aw_set_wavefield
 };
 
 namespace {
@@ -302,6 +324,53 @@ void lin_to_local(const aw_grid* g, int64_t lin, int64_t* zl, int64_t* uoff, int
     *uoff = *moff + (int64_t)g->R * g->geom.plane;
 }
 
+
+// Injection CSR over this rank's owned corners of n points: entries sorted by
+// corner (global linear index) ascending, then point index, then corner bit pattern.  Used for the
+// sources and, in the FWI adjoint (NEXT-3), for the receivers injecting the residual.
+struct E {
+    int64_t lin;
+    int s, beta;
+};
+struct InjTables {
+    std::vector<E> ents;
+    std::vector<int64_t> off, moff, lin;   // per unique corner: buffer offset; per entry: model offset
+    std::vector<int> plane, ptr, src, ent_src, ent_beta;
+    std::vector<double> w;
+};
+void build_injection(const aw_grid* g, int n, const std::vector<int64_t>& corner, const std::vector<double>& w,
+                     InjTables* t) {
+    const int nc = 1 << g->ndim;
+    for (int s = 0; s < n; ++s)
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t lin = corner[(size_t)s * nc + beta];
+            if (lin < 0) continue;
+            int64_t z = lin / lin_div(g);
+            if (z < g->z0 || z >= g->z0 + g->geom.nz) continue;
+            t->ents.push_back({lin, s, beta});
+        }
+    std::stable_sort(t->ents.begin(), t->ents.end(), [](const E& a, const E& b) {
+        return a.lin != b.lin ? a.lin < b.lin : (a.s != b.s ? a.s < b.s : a.beta < b.beta);
+    });
+    const std::vector<E>& ents = t->ents;
+    for (size_t e = 0; e < ents.size(); ++e) {
+        int64_t zl, uoff, moff;
+        lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
+        if (e == 0 || ents[e].lin != ents[e - 1].lin) {
+            t->off.push_back(uoff);
+            t->plane.push_back((int)zl);
+            t->ptr.push_back((int)e);
+            t->lin.push_back(ents[e].lin);
+        }
+        t->moff.push_back(moff);
+        t->src.push_back(ents[e].s);
+        t->w.push_back(w[(size_t)ents[e].s * nc + ents[e].beta]);
+        t->ent_src.push_back(ents[e].s);
+        t->ent_beta.push_back(ents[e].beta);
+    }
+    t->ptr.push_back((int)ents.size());
+}
+
 unsigned long long enc(const aw_grid* g, int64_t level) {
     return (g->epoch << 32) + (unsigned long long)(level + 1);
 }
@@ -332,6 +401,8 @@ void free_receivers(aw_grid* g) {  // views into g->rec_arena
     g->nr = g->rec_nt = g->nrl = 0;
     g->rec_corner_lin.clear();
     g->rec_w32.clear();
+    g->rec_w64.clear();
+    g->adj_valid = false;
 }
 
 template <class T>
@@ -465,7 +536,8 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0
         CK(aw::launch_stencil_stream(g->plan, g->geom, g->coefs, cur, g->ubuf[cur], g->ubuf[nxt], g->b,
                                      g->have_damp ? g->a : nullptr, g->halo, nxt, sp, g->d_base, i, g->s));
     } else {
-        CK(aw::launch_stencil_v1(g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->b, g->have_damp ? g->a : nullptr,
+        CK(aw::launch_stencil_v1(g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->ubuf[nxt], g->b,
+                                 g->have_damp ? g->a : nullptr,
                                  g->halo, nxt, g->s));
     }
     ++*launches;
@@ -642,6 +714,73 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     return AW_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// NEXT-3: adjoint-state FWI gradient (host orchestration; kernels in aw_fwi.cu)
+// ---------------------------------------------------------------------------
+
+// Adjoint injection tables: the receivers inject the residual like sources (DESIGN.md §3 Q24), so
+// their corners get the source treatment -- CSR by corner then receiver, scales
+// s = fl32(w64 dt^2 / (m_c + eta_c dt/2)) (computed on the device per call).
+aw_status fwi_build_adjoint(aw_grid* g) {
+    if (g->adj_valid) return AW_OK;
+    InjTables t;
+    build_injection(g, g->nr, g->rec_corner_lin, g->rec_w64, &t);
+    g->h_adj_lin = t.lin;
+    g->h_adj_ptr = t.ptr;
+    g->adj_nuc = (int)t.off.size();
+    g->adj_nent = (int)t.ents.size();
+    Packer pk;
+    const size_t o_off = pk.add(t.off), o_plane = pk.add(t.plane), o_ptr = pk.add(t.ptr), o_src = pk.add(t.src),
+                 o_moff = pk.add(t.moff), o_w = pk.add(t.w);
+    const size_t small = pk.off;
+    const size_t o_s = pk.reserve((size_t)g->adj_nent * sizeof(float));
+    aw_status st = ensure_arena(g, &g->adj_arena, &g->adj_cap, pk.off);
+    if (st) return st;
+    char* A = g->adj_arena;
+    g->d_adj_off = (int64_t*)(A + o_off);
+    g->d_adj_plane = (int*)(A + o_plane);
+    g->d_adj_ptr = (int*)(A + o_ptr);
+    g->d_adj_src = (int*)(A + o_src);
+    g->d_adj_moff = (int64_t*)(A + o_moff);
+    g->d_adj_w64 = (double*)(A + o_w);
+    g->d_adj_s = (float*)(A + o_s);
+    CK(cudaMemcpyAsync(A, pk.host.data(), small, cudaMemcpyHostToDevice, g->s));
+    CK(cudaStreamSynchronize(g->s));  // pk.host dies here
+    g->adj_valid = true;
+    return AW_OK;
+}
+
+// Checkpoint schedule: segments of K steps; the history ring holds the K+2 levels of one segment,
+// every later segment start keeps its two levels (u^{jK-1}, u^{jK}).  Buffers: K + 2 + 2(nseg - 1).
+int64_t fwi_buffers(int nt, int K) { return (int64_t)K + 2 + 2 * ((int64_t)(nt + K - 1) / K - 1); }
+
+int fwi_choose_K(const aw_grid* g, int nt, int64_t max_bufs) {
+    if (g->opt_ckpt > 0) return std::min(g->opt_ckpt, nt);
+    for (int K = nt; K >= 1; --K)  // largest segment that fits: fewest recomputed steps (nt - K)
+        if (fwi_buffers(nt, K) <= max_bufs) return K;
+    return 0;
+}
+
+// One time step on explicit buffers (history ring or adjoint pair); single slab.
+aw_status fwi_step(aw_grid* g, const float* ucur, const float* uprev, float* unext, const aw::Sparse& sp, int inj_set,
+                   int step_i, int64_t* launches) {
+    const float* a = g->have_damp ? g->a : nullptr;
+    if (g->kernel_used == AW_KERNEL_STREAM) {
+        CK(aw::launch_stencil_stream_bufs(g->plan, g->geom, g->coefs, ucur, uprev, unext, g->b, a, sp, inj_set,
+                                          g->d_base, step_i, g->s));
+        ++*launches;
+    } else {
+        Halo none{};
+        CK(aw::launch_stencil_v1(g->geom, g->coefs, ucur, uprev, unext, g->b, a, none, 0, g->s));
+        ++*launches;
+        if (sp.nrl + sp.nuc > 0) {
+            CK(aw::launch_sparse_step(g->geom, sp, ucur, unext, g->d_base, step_i, none, 0, g->s));
+            ++*launches;
+        }
+    }
+    return AW_OK;
+}
 }  // namespace
 
 // ===========================================================================
@@ -792,6 +931,9 @@ void aw_grid_destroy(aw_grid* g) {
     free_receivers(g);
     dfree(g->src_arena);
     dfree(g->rec_arena);
+    dfree(g->adj_arena);
+    dfree(g->fwi_arena);
+    dfree(g->fwi_pool);
     dfree(g->ubuf[0]);
     dfree(g->ubuf[1]);
     dfree(g->m);
@@ -878,49 +1020,17 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
     g->src_corner_lin = corner;
     g->src_w64 = w;
     // owned entries in CSR order: corner ascending, then source ascending (Q11)
-    struct E {
-        int64_t lin;
-        int s, beta;
-    };
-    std::vector<E> ents;
-    for (int s = 0; s < ns; ++s)
-        for (int beta = 0; beta < nc; ++beta) {
-            int64_t lin = corner[(size_t)s * nc + beta];
-            if (lin < 0) continue;
-            int64_t z = lin / lin_div(g);
-            if (z < g->z0 || z >= g->z0 + g->geom.nz) continue;
-            ents.push_back({lin, s, beta});
-        }
-    std::stable_sort(ents.begin(), ents.end(), [](const E& a, const E& b) {
-        return a.lin != b.lin ? a.lin < b.lin : (a.s != b.s ? a.s < b.s : a.beta < b.beta);
-    });
-    std::vector<int64_t> inj_off, inj_moff;
-    std::vector<int> inj_plane, inj_ptr, inj_src;
-    std::vector<double> inj_w;
-    for (size_t e = 0; e < ents.size(); ++e) {
-        if (e == 0 || ents[e].lin != ents[e - 1].lin) {
-            int64_t zl, uoff, moff;
-            lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
-            inj_off.push_back(uoff);
-            inj_plane.push_back((int)zl);
-            inj_ptr.push_back((int)e);
-            g->h_inj_lin.push_back(ents[e].lin);
-        }
-        int64_t zl, uoff, moff;
-        lin_to_local(g, ents[e].lin, &zl, &uoff, &moff);
-        inj_moff.push_back(moff);
-        inj_src.push_back(ents[e].s);
-        inj_w.push_back(w[(size_t)ents[e].s * nc + ents[e].beta]);
-        g->ent_src.push_back(ents[e].s);
-        g->ent_beta.push_back(ents[e].beta);
-    }
-    inj_ptr.push_back((int)ents.size());
-    g->h_inj_ptr = inj_ptr;
-    g->nuc = (int)inj_off.size();
-    g->nent = (int)ents.size();
+    InjTables t;
+    build_injection(g, ns, corner, w, &t);
+    g->h_inj_lin = t.lin;
+    g->h_inj_ptr = t.ptr;
+    g->ent_src = t.ent_src;
+    g->ent_beta = t.ent_beta;
+    g->nuc = (int)t.off.size();
+    g->nent = (int)t.ents.size();
     Packer pk;
-    const size_t o_off = pk.add(inj_off), o_plane = pk.add(inj_plane), o_ptr = pk.add(inj_ptr),
-                 o_src = pk.add(inj_src), o_moff = pk.add(inj_moff), o_w = pk.add(inj_w);
+    const size_t o_off = pk.add(t.off), o_plane = pk.add(t.plane), o_ptr = pk.add(t.ptr), o_src = pk.add(t.src),
+                 o_moff = pk.add(t.moff), o_w = pk.add(t.w);
     const size_t small = pk.off;
     const size_t o_s = pk.reserve((size_t)g->nent * sizeof(float));
     const size_t o_wav = pk.reserve((size_t)nt_max * ns * sizeof(float));
@@ -961,6 +1071,7 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
     g->rec_corner_lin = corner;
     g->rec_w32.resize(w.size());
     for (size_t i = 0; i < w.size(); ++i) g->rec_w32[i] = (float)w[i];
+    g->rec_w64 = w;
     // owner = rank owning the base corner's plane; its +1 corner may be a halo plane
     std::vector<int> ids;
     std::vector<int64_t> offs;
@@ -1030,16 +1141,201 @@ aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, 
     }
     CK(cudaStreamSynchronize(g->s));
     g->halo_dirty = team_mode(g) && layout == AW_LOCAL;
+    g->wave_invalid = false;
     return leave(g);
 }
 
 aw_status aw_run(aw_grid* g, int nt, double dt) {
     CHECK_STATE(g);
+    if (g->wave_invalid) return fail(AW_ESTATE, "call aw_reset (or aw_set_wavefield) after aw_fwi_gradient");
     aw_status st = run_begin(g, nt, dt);
     if (st) return st;
     int64_t launches = 0;
     if ((st = run_enqueue(g, nt, &launches))) return st;
     return run_end(g, nt, launches);
+}
+
+aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, float* grad, int layout,
+                          float* residual, double* objective) {
+    CHECK_STATE(g);
+    if (team_mode(g)) return fail(AW_EUNSUPPORTED, "aw_fwi_gradient runs on a single slab (world = 1)");
+    if (nt < 1) return fail(AW_EINVAL, "nt must be >= 1 (got %d)", nt);
+    if (!d_obs || !grad) return fail(AW_EINVAL, "d_obs/grad is NULL");
+    if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(AW_EINVAL, "dt must be finite and > 0");
+    if (!g->have_model) return fail(AW_ESTATE, "aw_set_model has not been called");
+    if (g->nr == 0) return fail(AW_EINVAL, "the misfit needs receivers (aw_add_receivers)");
+    if (g->ns > 0 && nt > g->src_nt) return fail(AW_EINVAL, "wavelet covers %d steps, need %d", g->src_nt, nt);
+    if (nt > g->rec_nt) return fail(AW_EINVAL, "trace buffer covers %d steps, need %d", g->rec_nt, nt);
+    aw_status st = enter(g);
+    if (st) return st;
+    // start from the reset state (zero wavefields, step 0) with this dt
+    g->steps = 0;
+    g->cur = 0;
+    if (!(g->dt_set && g->dt == dt)) g->coeffs_valid = false;  // any dt: the call starts from the reset state
+    if ((st = prepare(g, dt))) return st;
+    if ((st = fwi_build_adjoint(g))) return st;
+    CK(aw::launch_source_scales(g->m, g->have_damp ? g->eta : nullptr, g->d_adj_moff, g->d_adj_w64, g->d_adj_s,
+                                g->adj_nent, dt, g->s));
+    int64_t launches = g->adj_nent > 0 ? 1 : 0;
+    if (g->kernel_used == AW_KERNEL_STREAM) {
+        cudaError_t e = aw::stream_set_injection(g->plan, g->geom, g->z0, g->h_adj_lin.data(), g->h_adj_ptr.data(),
+                                                 g->adj_nuc, g->s, 1);
+        CK(e);
+    }
+
+    // ---- memory: per-call arrays and the history/checkpoint pool (kept between calls) ----
+    const int nr = g->nr;
+    const size_t tr = (size_t)nt * nr * sizeof(float);
+    const size_t fwi_bytes = 3 * ((tr + 255) / 256 * 256) + 256 + g->mbytes;
+    if ((st = ensure_arena(g, &g->fwi_arena, &g->fwi_cap, fwi_bytes))) return st;
+    float* d_dobs = (float*)g->fwi_arena;
+    float* d_res = (float*)(g->fwi_arena + (tr + 255) / 256 * 256);
+    float* d_wadj = (float*)(g->fwi_arena + 2 * ((tr + 255) / 256 * 256));
+    double* d_J = (double*)(g->fwi_arena + 3 * ((tr + 255) / 256 * 256));
+    float* d_G = (float*)(g->fwi_arena + 3 * ((tr + 255) / 256 * 256) + 256);
+    {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        const int64_t have = g->fwi_pool_nbuf;
+        const int64_t max_bufs = have + (int64_t)((double)fr * 0.6 / (double)g->ubytes);
+        const int K = fwi_choose_K(g, nt, max_bufs);
+        if (K < 1) return fail(AW_ENOMEM, "not enough device memory for the FWI history (%lld buffers of %zu B)",
+                               (long long)fwi_buffers(nt, 1), g->ubytes);
+        const int64_t need = fwi_buffers(nt, K);
+        if (need > have) {
+            if (g->fwi_pool) {
+                CK(cudaStreamSynchronize(g->s));
+                cudaFree(g->fwi_pool);
+                g->fwi_pool = nullptr;
+                g->fwi_pool_nbuf = 0;
+            }
+            cudaError_t e = cudaMalloc((void**)&g->fwi_pool, (size_t)need * g->ubytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(AW_ENOMEM, "FWI history pool of %lld buffers: %s", (long long)need, cudaGetErrorString(e));
+            }
+            g->fwi_pool_nbuf = need;
+            CK(cudaMemsetAsync(g->fwi_pool, 0, (size_t)need * g->ubytes, g->s));  // zero halo planes for good
+        }
+        g->stats.fwi_checkpoint = K;
+    }
+    const int K = g->stats.fwi_checkpoint;
+    const int nseg = (nt + K - 1) / K;
+    const int S = K + 2;
+    const int64_t ufl = (int64_t)(g->ubytes / sizeof(float));
+    const int64_t own_off = (int64_t)g->R * g->geom.plane;                // first owned plane
+    const size_t own_bytes = (size_t)g->geom.nz * g->geom.plane * sizeof(float);
+    float* pool = g->fwi_pool;
+    auto slot = [&](int64_t level) { return pool + (((level + 1) % S + S) % S) * ufl; };  // level -1 .. nt
+    auto ckpt = [&](int j, int which) { return pool + ((int64_t)S + 2 * (j - 1) + which) * ufl; };  // j >= 1
+    auto zero_level = [&](int64_t level) -> aw_status {
+        CK(cudaMemsetAsync(slot(level) + own_off, 0, own_bytes, g->s));
+        return AW_OK;
+    };
+    auto copy_level = [&](float* dst, const float* src) -> aw_status {
+        CK(cudaMemcpyAsync(dst + own_off, src + own_off, own_bytes, cudaMemcpyDeviceToDevice, g->s));
+        return AW_OK;
+    };
+
+    CK(cudaEventRecord(g->ev_t0, g->s));
+    const int64_t zero = 0;
+    CK(cudaMemcpyAsync(g->d_base, &zero, sizeof zero, cudaMemcpyHostToDevice, g->s));
+    CK(cudaMemcpyAsync(d_dobs, d_obs, tr, ptr_kind(d_obs) == PK_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                      : cudaMemcpyHostToDevice, g->s));
+    if (g->d_traces) CK(cudaMemsetAsync(g->d_traces, 0, (size_t)g->rec_nt * nr * sizeof(float), g->s));
+    int64_t steps_done = 0;
+    aw::Sparse fwd = sparse_view(g);  // sources + receivers (first pass)
+    aw::Sparse fwd_norec = fwd;       // recompute: sources only (traces already recorded)
+    fwd_norec.nrl = 0;
+    aw::Sparse adj{};                 // adjoint: the receivers inject the time-reversed residual
+    adj.nuc = g->adj_nuc;
+    adj.ns = nr;
+    adj.inj_off = g->d_adj_off;
+    adj.inj_plane = g->d_adj_plane;
+    adj.inj_ptr = g->d_adj_ptr;
+    adj.inj_src = g->d_adj_src;
+    adj.inj_s = g->d_adj_s;
+    adj.wavelet = d_wadj;
+    adj.nc = 1 << g->ndim;
+
+    // ---- 1. forward pass into the history ring; checkpoints at segment starts ----
+    if ((st = zero_level(-1)) || (st = zero_level(0))) return st;
+    for (int n = 0; n < nt; ++n) {
+        if ((st = fwi_step(g, slot(n), slot(n - 1), slot(n + 1), fwd, 0, n, &launches))) return st;
+        ++steps_done;
+        const int l = n + 1;
+        if (l % K == 0 && l < nt) {  // level jK of segment j = l/K >= 1: keep (u^{jK-1}, u^{jK})
+            const int j = l / K;
+            if ((st = copy_level(ckpt(j, 0), slot(l - 1))) || (st = copy_level(ckpt(j, 1), slot(l)))) return st;
+        }
+    }
+    // ---- 2. residual, misfit, adjoint wavelet ----
+    CK(aw::launch_fwi_residual(g->d_traces, d_dobs, d_res, d_wadj, nt, nr, d_J, g->s));
+    ++launches;
+    // ---- 3. adjoint run in reversed time, segment by segment, imaging before each step ----
+    float* psi[2] = {g->ubuf[0], g->ubuf[1]};
+    CK(cudaMemsetAsync(psi[0], 0, g->ubytes, g->s));
+    CK(cudaMemsetAsync(psi[1], 0, g->ubytes, g->s));
+    CK(cudaMemsetAsync(d_G, 0, g->mbytes, g->s));
+    int pc = 0;  // psi^k in psi[pc], psi^{k-1} in psi[1-pc]
+    for (int j = nseg - 1; j >= 0; --j) {
+        const int lo = j * K, hi = std::min(lo + K, nt);
+        if (j < nseg - 1) {  // recompute levels lo+1 .. hi from the checkpoint
+            if (j == 0) {
+                if ((st = zero_level(-1)) || (st = zero_level(0))) return st;
+            } else if ((st = copy_level(slot(lo - 1), ckpt(j, 0))) || (st = copy_level(slot(lo), ckpt(j, 1)))) {
+                return st;
+            }
+            for (int n = lo; n < hi; ++n) {
+                if ((st = fwi_step(g, slot(n), slot(n - 1), slot(n + 1), fwd_norec, 0, n, &launches))) return st;
+                ++steps_done;
+            }
+        }
+        for (int n = hi - 1; n >= lo; --n) {
+            const int k = nt - 1 - n;
+            CK(aw::launch_fwi_imaging(g->geom, psi[pc], slot(n + 1), slot(n), slot(n - 1), d_G, g->s));
+            ++launches;
+            if (k == nt - 1) break;  // psi^nt pairs with no forward level
+            if ((st = fwi_step(g, psi[pc], psi[1 - pc], psi[1 - pc], adj, 1, k, &launches))) return st;
+            ++steps_done;
+            pc = 1 - pc;
+        }
+    }
+    // ---- 4. gradient = -G / dt^2, outputs ----
+    CK(aw::launch_fwi_finalize(g->geom, d_G, dt, g->s));
+    ++launches;
+    CK(cudaEventRecord(g->ev_t1, g->s));
+    {
+        const int64_t nx = g->geom.nx, ny = g->geom.ny;
+        float* dst = layout == AW_GLOBAL ? grad + g->z0 * ny * nx : grad;
+        if ((st = copy_out(g, dst, d_G, g->geom.pitch, nx, (int64_t)g->geom.nz * ny))) return st;
+    }
+    if (residual)
+        CK(cudaMemcpyAsync(residual, d_res, tr, ptr_kind(residual) == PK_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                                : cudaMemcpyDeviceToHost, g->s));
+    double J = 0.0;
+    CK(cudaMemcpyAsync(&J, d_J, sizeof J, cudaMemcpyDeviceToHost, g->s));
+    if ((st = leave(g))) return st;
+    CK(cudaStreamSynchronize(g->s));
+    if (objective) *objective = J;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, g->ev_t0, g->ev_t1));
+    g->stats.ms_total = ms;
+    g->stats.ms_stencil = -1.0;
+    g->stats.n_stencil = 0;
+    g->stats.launches = launches;
+    g->launch_count += launches;
+    g->stats.launches_total = g->launch_count;
+    g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
+    g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
+    g->stats.kernel = g->kernel_used;
+    g->stats.fwi_steps = steps_done;
+    // the traces of the forward run stay readable; the wavefield levels hold the adjoint field
+    g->steps = nt;
+    g->wave_invalid = true;
+    if (!std::isfinite(J)) return fail(AW_ENONFINITE, "misfit is not finite (J = %g)", J);
+    return AW_OK;
 }
 
 aw_status aw_reset(aw_grid* g) {
@@ -1053,6 +1349,7 @@ aw_status aw_reset(aw_grid* g) {
     g->cur = 0;
     g->dt_set = false;
     g->coeffs_valid = false;
+    g->wave_invalid = false;
     if (team_mode(g)) {
         // after my memsets: neighbours may start storing level-1 halos into my buffers
         g->epoch += 1;
@@ -1068,6 +1365,7 @@ aw_status aw_read_wavefield(aw_grid* g, int which, float* out, int layout) {
     if (!out) return fail(AW_EINVAL, "out is NULL");
     if (which != 0 && which != 1) return fail(AW_EINVAL, "which must be 0 or 1");
     if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
+    if (g->wave_invalid) return fail(AW_ESTATE, "no forward wavefield after aw_fwi_gradient (aw_reset first)");
     aw_status st = enter(g);
     if (st) return st;
     const float* buf = g->ubuf[which == 0 ? g->cur : 1 - g->cur];
@@ -1146,6 +1444,10 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
             return AW_OK;
         case AW_OPT_CHECK_FINITE:
             g->opt_check = value != 0;
+            return AW_OK;
+        case AW_OPT_CHECKPOINT_STEPS:
+            if (value < 0 || value > (1 << 30)) return fail(AW_EINVAL, "checkpoint steps out of range");
+            g->opt_ckpt = (int)value;
             return AW_OK;
         default:
             return fail(AW_EINVAL, "unknown option %d", option);

@@ -64,7 +64,9 @@ cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& 
                                   cudaStream_t s);
 cudaError_t launch_source_scales(const float* m, const float* eta, const int64_t* moff, const double* w64,
                                  float* s_out, int nent, double dt, cudaStream_t s);
-cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, float* unext,
+// uprev = u^{n-1}: unext itself for the in-place two-buffer time loop, or another buffer
+// (FWI history ring, NEXT-3)
+cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, const float* uprev, float* unext,
                               const float* b, const float* a, const Halo& halo, int parity_next,
                               cudaStream_t s);
 cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucur, float* unext,
@@ -93,7 +95,25 @@ cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, 
                                   const float* ucur, float* unext, const float* b, const float* a,
                                   const Halo& halo, int parity_next, const Sparse& sp, const int64_t* d_base,
                                   int step_i, cudaStream_t s);
+// injection lists per tile-plane; set 0 = the sources, set 1 = the FWI adjoint sources (receivers)
 cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const int64_t* corner_lin, const int* ptr,
-                                 int nuc, cudaStream_t s);
+                                 int nuc, cudaStream_t s, int set = 0);
+// One step on explicit buffers (u^n = ucur, u^{n-1} = uprev, u^{n+1} -> unext; single slab, no team):
+// the tensor maps are encoded for these buffers at launch.  inj_set selects the injection lists.
+cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const float* ucur,
+                                       const float* uprev, float* unext, const float* b, const float* a,
+                                       const Sparse& sp, int inj_set, const int64_t* d_base, int step_i,
+                                       cudaStream_t s);
+
+// ---- NEXT-3 FWI kernels (aw_fwi.cu) ----
+// G += psi * D,  D = fl32(fl32(u1 - 2 u0) + um1), over the owned planes (wavefield layout inputs,
+// model layout G)
+cudaError_t launch_fwi_imaging(const Geom& g, const float* psi, const float* u1, const float* u0, const float* um1,
+                               float* G, cudaStream_t s);
+// res[n][r] = fl32(rec - d_obs); wadj[nt-1-n][r] = res[n][r]; *J = 0.5 sum res^2 (fp64, fixed order)
+cudaError_t launch_fwi_residual(const float* rec, const float* dobs, float* res, float* wadj, int nt, int nr,
+                                double* J, cudaStream_t s);
+// grad = fl32(-(double)G / dt^2) in place (model layout, padding stays 0)
+cudaError_t launch_fwi_finalize(const Geom& g, float* G, double dt, cudaStream_t s);
 
 }  // namespace aw

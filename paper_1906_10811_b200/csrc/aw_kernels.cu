@@ -108,7 +108,7 @@ cudaError_t launch_source_scales(const float* m, const float* eta, const int64_t
 // ---------------------------------------------------------------------------
 template <int NDIM, int R>
 __global__ void __launch_bounds__(256) stencil_v1_kernel(Geom g, Coefs c, const float* __restrict__ ucur,
-                                                         float* __restrict__ unext, const float* __restrict__ b,
+                                                         const float* uprev, float* unext, const float* __restrict__ b,
                                                          const float* __restrict__ a, float* __restrict__ lo,
                                                          int64_t lo_off, float* __restrict__ hi, int64_t hi_off) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) stencil_v1_kernel(Geom g, Coefs c, const 
 #pragma unroll
     for (int j = 1; j <= R; ++j)
         L = __fmaf_rn(c.C[0][j], __fadd_rn(p[-(int64_t)j * g.plane], p[(int64_t)j * g.plane]), L);
-    const float um = unext[ou];  // u^{n-1} lives in the output buffer (in place)
+    const float um = uprev[ou];  // u^{n-1}: the output buffer itself (in place) or a history level
     const float t = __fsub_rn(__fmul_rn(2.0f, uc), um);
     const float w = __fmaf_rn(b[o], L, t);
     const float aa = a ? a[o] : 1.0f;
@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(256) stencil_v1_kernel(Geom g, Coefs c, const 
 }
 
 template <int NDIM>
-static cudaError_t launch_v1_ndim(const Geom& g, const Coefs& c, const float* ucur, float* unext, const float* b,
+static cudaError_t launch_v1_ndim(const Geom& g, const Coefs& c, const float* ucur, const float* uprev, float* unext,
+                                  const float* b,
                                   const float* a, float* lo, int64_t lo_off, float* hi, int64_t hi_off,
                                   cudaStream_t s) {
     dim3 block, grid;
@@ -165,7 +166,7 @@ static cudaError_t launch_v1_ndim(const Geom& g, const Coefs& c, const float* uc
     }
     switch (g.R) {
 #define AW_CASE(RR) \
-    case RR: stencil_v1_kernel<NDIM, RR><<<grid, block, 0, s>>>(g, c, ucur, unext, b, a, lo, lo_off, hi, hi_off); break;
+    case RR: stencil_v1_kernel<NDIM, RR><<<grid, block, 0, s>>>(g, c, ucur, uprev, unext, b, a, lo, lo_off, hi, hi_off); break;
         AW_CASE(1) AW_CASE(2) AW_CASE(3) AW_CASE(4) AW_CASE(5) AW_CASE(6) AW_CASE(7) AW_CASE(8)
 #undef AW_CASE
         default: return cudaErrorInvalidValue;
@@ -173,12 +174,12 @@ static cudaError_t launch_v1_ndim(const Geom& g, const Coefs& c, const float* uc
     return cudaGetLastError();
 }
 
-cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, float* unext, const float* b,
-                              const float* a, const Halo& halo, int parity_next, cudaStream_t s) {
+cudaError_t launch_stencil_v1(const Geom& g, const Coefs& c, const float* ucur, const float* uprev, float* unext,
+                              const float* b, const float* a, const Halo& halo, int parity_next, cudaStream_t s) {
     float* lo = halo.lo[parity_next];
     float* hi = halo.hi[parity_next];
-    if (g.ndim == 3) return launch_v1_ndim<3>(g, c, ucur, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
-    return launch_v1_ndim<2>(g, c, ucur, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
+    if (g.ndim == 3) return launch_v1_ndim<3>(g, c, ucur, uprev, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
+    return launch_v1_ndim<2>(g, c, ucur, uprev, unext, b, a, lo, halo.lo_off, hi, halo.hi_off, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -1,440 +1,14 @@
-// aw_stream.cu -- 2.5D z-streaming stencil kernel for 3D grids (sm_100a).
-//
-// The hot loop of the path (SURVEY.md §8(a) rows a5+a6): star Laplacian of
-// order k = 2R fused with the damped leapfrog update.  It is HBM-bound at
-// 16 algorithmic B per point update, so the design goal is to
-// stream u^n, u^{n-1}, b (and a where eta != 0) exactly once from HBM and
-// write u^{n+1} once, with few enough instructions per point that the SMs
-// keep up with HBM.  B200-first choices (not the paper's OPS-generated code):
-//
-//  * persistent grid of (#SMs x resident CTAs) CTAs; work items are
-//    (xy tile, z chunk) pairs handed out cyclically, so at any time the
-//    resident CTAs work on neighbouring tiles at the same z and the halo rows
-//    one CTA loads are L2 hits for its neighbours;
-//  * one producer warp issues TMA (cp.async.bulk.tensor.3d) loads of the u^n
-//    plane tile with its halo into a ring of SU = R+1+D shared-memory stages
-//    (full/empty mbarriers), plus TMA L2 prefetches PD planes ahead for every
-//    stream the consumers read (u^n tiles, and the u^{n-1}, b, a tiles of
-//    the output planes).  TMA's out-of-bounds zero fill is the zero-ghost
-//    boundary in x and y; z ghosts are zeroed halo planes;
-//  * consumer warps: lane l owns the x columns x0+l and x0+l+32 of RY rows,
-//    so every operation is done on point pairs with the Blackwell packed-fp32
-//    instructions (FFMA2/FADD2/FMUL2, per-lane IEEE RN == the scalar ops);
-//  * z neighbours come from a register queue of 2R+1 centre values; the
-//    plane loop is unrolled by 2R+1 so the queue rotates by renaming, not by
-//    moves; x and y neighbours come from the resident stage of the output
-//    plane (the y column is loaded once per thread and shared by its rows);
-//  * interior tiles run a predicate-free path; edge tiles mask their loads
-//    and stores;
-//  * in a team, boundary planes are also stored into the neighbours' halo
-//    planes (peer memory over NVLink): the fused exchange.
-//
-// Per point the arithmetic is the canonical sequence of SURVEY §8(c).6:
-//   L = C0*u; x pairs j=1..R; y pairs; z pairs (fma each); t = 2u - u^{n-1};
-//   w = fma(b, L, t); u^{n+1} = fma(a, w, (1-a) u^{n-1})
-// so the result is value-identical to the fp32 oracle and the v1 kernel.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
+// aw_stream.cu -- host side of the 2.5D z-streaming stencil kernel (R-independent):
+// plan construction, eta flags, injection lists, dispatch to the per-R translation units
+// (aw_stream_r{1..8}.cu; the kernel itself is in aw_stream.cuh).
 #include <algorithm>
 #include <cstdlib>
-#include <cstring>
 #include <utility>
 #include <vector>
 
-#include "aw_internal.h"
+#include "aw_stream.cuh"
 
 namespace aw {
-
-namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(addr),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-                 "r"(c2)
-                 : "memory");
-}
-__device__ __forceinline__ float ldg_stream(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-
-// packed fp32 (Blackwell FFMA2/FADD2/FMUL2): per component identical to the scalar _rn ops
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-
-template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_>
-struct Cfg {
-    static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
-    static constexpr int Q = 2 * R + 1;  // z queue length (and plane-loop unroll)
-    // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
-    // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
-    static constexpr int RP = (R + 3) / 4 * 4;
-    static constexpr int TXP = TX + 2 * RP;
-    static constexpr int TYP = TY + 2 * R;
-    static constexpr int SU = R + 1 + D;  // u^n ring: planes [p-R, p+D]
-    static constexpr int SP = DP + 1;     // (u^{n-1}, b, a) ring of the output planes
-    static constexpr int NWARPS_COMP = TY / RY;
-    static constexpr int NCOMP = 32 * NWARPS_COMP;
-    static constexpr int NTHREADS = NCOMP + 96;  // + u^n producer, streams producer, receivers warp
-    static constexpr int STAGE_FLOATS = TXP * TYP;
-    static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;                 // TMA transaction bytes
-    static constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;  // 128-B aligned ring slots
-    static constexpr int STAGE_STRIDE_F = STAGE_STRIDE / 4;
-    static constexpr int PTILE_FLOATS = TX * TY;
-    static constexpr int PTILE_BYTES = PTILE_FLOATS * 4;
-    static constexpr int PSTAGE_FLOATS = 3 * PTILE_FLOATS;  // u^{n-1}, b, a
-    static constexpr size_t U_BYTES = (size_t)SU * STAGE_STRIDE;
-    static constexpr size_t P_BYTES = (size_t)SP * PSTAGE_FLOATS * 4;
-    // + full/empty barriers of both rings + 3 metadata words per streams stage
-    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + 3 * SP * sizeof(int);
-    static_assert(TY % RY == 0, "tile shape");
-    static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
-};
-
-struct StreamArgs {
-    Geom g;
-    Coefs c;
-    float* unext;            // buffer base (plane -R)
-    const float* a;          // may be null (no damping)
-    const uint8_t* flags;    // [ntiles][nz]: 1 if any a != 1 in the tile-plane
-    float* lo;               // team halo targets (null if none)
-    int64_t lo_off;
-    float* hi;
-    int64_t hi_off;
-    int ntx, nty;            // tiles along x, y
-    int nzc, zc;             // z chunks and planes per chunk
-    int nitems;              // ntiles * nzc
-    // fused per-step sparse work (SURVEY §8(a) a7 injection, a8 receivers)
-    const int2* tpsc;        // [ntiles][nz]: {first entry, count} of injection corners in the tile-plane
-    const int4* tpe;         // entries: {tile-local point ly*64+lx, csr begin, csr end, 0}
-    const int* inj_src;      // [nent] source index (CSR: corner ascending, then source)
-    const float* inj_s;      // [nent] fp32 scale dt^2 w / (m + eta dt/2)
-    const float* wavelet;    // [nt_max][ns]
-    int ns;
-    int nrl, nr, nc;         // owned receivers, trace row length, corners per point
-    const int* rec_id;
-    const int64_t* rec_off;  // element offsets into the u^n buffer (-1: skipped corner)
-    const float* rec_w;
-    float* traces;           // [nt_max][nr]
-    const float* ucur;       // u^n buffer base (plane -R)
-    const int64_t* d_base;   // the step index is n = *d_base + step_i (graph-replay friendly)
-    int step_i;
-};
-
-struct StreamMaps {
-    CUtensorMap u;    // u^n buffer, box (TXP, TYP, 1): ring loads + L2 prefetch
-    CUtensorMap un;   // u^{n-1}/u^{n+1} buffer, box (TX, TY, 1)
-    CUtensorMap b;    // model layout, box (TX, TY, 1)
-    CUtensorMap a;    // model layout, box (TX, TY, 1) (b again when there is no damping)
-};
-
-struct Ring {
-    uint32_t slot, phase;
-    __device__ __forceinline__ void advance(uint32_t n) {
-        if (++slot == n) {
-            slot = 0;
-            phase ^= 1;
-        }
-    }
-};
-
-}  // namespace
-
-// One work item (xy tile, z chunk) for a consumer thread.  INTERIOR tiles need
-// no bounds predicates.  The ring positions advance exactly like the producer's.
-template <class C, bool INTERIOR, bool TEAM>
-__device__ __forceinline__ void consume_item(const StreamArgs& A, const float* ring, const float* pring,
-                                             uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
-                                             const volatile int* pmeta,
-                                             int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
-                                             Ring& rp, int64_t step_n) {
-    constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
-    const Geom& g = A.g;
-    const int nz = g.nz;
-    const int ntiles = A.ntx * A.nty;
-    const int niter = ze - zb + 2 * R;
-    const int64_t pitch = g.pitch, plane = g.plane;
-    const float2 C0 = f2(A.c.C0, A.c.C0);
-    const float2 two = f2(2.0f, 2.0f), one = f2(1.0f, 1.0f);
-    const int xa = x0 + lane, xb = x0 + lane + 32;
-    const bool inA = INTERIOR || xa < g.nx, inB = INTERIOR || xb < g.nx;
-    bool ok_a[RY], ok_b[RY];
-#pragma unroll
-    for (int i = 0; i < RY; ++i) {
-        const bool r = INTERIOR || (y0 + ly + i) < g.ny;
-        ok_a[i] = inA && r;
-        ok_b[i] = inB && r;
-    }
-    // u^{n+1} of (z, y0+ly, xa): advanced by `plane` per output plane
-    float* outp = A.unext + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
-
-    float2 q[RY][Q];
-#pragma unroll
-    for (int i = 0; i < RY; ++i)
-#pragma unroll
-        for (int j = 0; j < Q; ++j) q[i][j] = f2(0.0f, 0.0f);
-
-    for (int kb = 0; kb < niter; kb += Q) {
-#pragma unroll
-        for (int uq = 0; uq < Q; ++uq) {
-            const int k = kb + uq;
-            if (k >= niter) break;
-            mbar_wait(&fullU[ru.slot], ru.phase);
-            const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + lane;
-            // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
-#pragma unroll
-            for (int i = 0; i < RY; ++i) q[i][uq] = f2(P[i * TXP], P[i * TXP + 32]);
-            const uint32_t slotR = ru.slot >= (uint32_t)R ? ru.slot - R : ru.slot + SU - R;  // plane p-R
-            if (k >= 2 * R) {
-                const int z = zb + k - 2 * R;  // output plane
-                const float* Qs = ring + slotR * C::STAGE_STRIDE_F + ly * TXP + RP + lane;
-                // (u^{n-1}, b, a) tiles of the output plane
-                mbar_wait(&fullP[rp.slot], rp.phase);
-                const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + lane;
-                // stage metadata written by the streams producer before its arrive: use_a, injection list
-                const bool use_a = pmeta[3 * rp.slot] != 0;
-                const int inj_first = pmeta[3 * rp.slot + 1], inj_count = pmeta[3 * rp.slot + 2];
-                // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
-                float2 col[RY + 2 * R];
-#pragma unroll
-                for (int r = 0; r < RY + 2 * R; ++r) col[r] = f2(Qs[r * TXP], Qs[r * TXP + 32]);
-                float2 res[RY];
-#pragma unroll
-                for (int i = 0; i < RY; ++i) {
-                    const float* row = Qs + (i + R) * TXP;
-                    const float2 uc = q[i][(uq + Q - R) % Q];
-                    float2 L = mul2(C0, uc);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = fma2(f2(A.c.C[2][j], A.c.C[2][j]),
-                                 add2(f2(row[-j], row[32 - j]), f2(row[j], row[32 + j])), L);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = fma2(f2(A.c.C[1][j], A.c.C[1][j]), add2(col[i + R - j], col[i + R + j]), L);
-#pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = fma2(f2(A.c.C[0][j], A.c.C[0][j]),
-                                 add2(q[i][(uq + Q - R - j) % Q], q[i][(uq + Q - R + j) % Q]), L);
-                    const float* pr = Pp + i * TX;
-                    const float2 um = f2(pr[0], pr[32]);
-                    const float2 bb = f2(pr[C::PTILE_FLOATS], pr[C::PTILE_FLOATS + 32]);
-                    const float2 aa = use_a ? f2(pr[2 * C::PTILE_FLOATS], pr[2 * C::PTILE_FLOATS + 32]) : one;
-                    // t = 2u - u^{n-1} (2u exact: one rounding), w = fma(b, L, t)
-                    const float2 t = fma2(two, uc, f2(-um.x, -um.y));
-                    const float2 wv = fma2(bb, L, t);
-                    const float2 rr = mul2(add2(one, f2(-aa.x, -aa.y)), um);
-                    res[i] = fma2(aa, wv, rr);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyP[rp.slot]);
-                rp.advance(SP);
-                // fused injection: u^{n+1}[c] = fma(s, q[n][src], u^{n+1}[c]) over the
-                // corner's sources in CSR order, applied by the thread that owns the corner, before storing
-                for (int e = inj_first; e < inj_first + inj_count; ++e) {
-                    const int4 en = A.tpe[e];
-                    const int yl = en.x >> 6, xl = en.x & 63;
-#pragma unroll
-                    for (int i = 0; i < RY; ++i) {
-                        if (yl != ly + i || (xl & 31) != lane) continue;
-                        float v = xl < 32 ? res[i].x : res[i].y;
-                        const float* qn = A.wavelet + step_n * A.ns;
-                        for (int k = en.y; k < en.z; ++k) v = __fmaf_rn(A.inj_s[k], qn[A.inj_src[k]], v);
-                        if (xl < 32) res[i].x = v; else res[i].y = v;
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < RY; ++i) {
-                    float* o = outp + i * pitch;
-                    if (ok_a[i]) o[0] = res[i].x;
-                    if (ok_b[i]) o[32] = res[i].y;
-                }
-                if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
-                    // fused exchange: boundary planes also go straight into the neighbour's halo
-                    const int64_t om = (outp - A.unext) - (int64_t)R * plane;  // model-layout index
-                    float* h = (A.lo && z < R) ? A.lo + A.lo_off + om
-                                               : A.hi + A.hi_off + om - (int64_t)(nz - R) * plane;
-#pragma unroll
-                    for (int i = 0; i < RY; ++i) {
-                        if (ok_a[i]) h[i * pitch] = res[i].x;
-                        if (ok_b[i]) h[i * pitch + 32] = res[i].y;
-                    }
-                }
-                outp += plane;
-            }
-            // release the stage of plane p - R (no longer needed by any later output)
-            if (k >= R) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyU[slotR]);
-            }
-            ru.advance(SU);
-        }
-    }
-    // release the last R stages of this item (planes ze .. ze+R-1)
-#pragma unroll 1
-    for (int m = 0; m < R; ++m) {
-        const uint32_t s = ru.slot >= (uint32_t)(R - m) ? ru.slot - (R - m) : ru.slot + SU - (R - m);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyU[s]);
-    }
-}
-
-template <class C, bool TEAM>
-__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
-    stream_kernel(const __grid_constant__ StreamMaps M, const __grid_constant__ StreamArgs A) {
-    constexpr int R = C::R, TX = C::TX, TY = C::TY, RP = C::RP, SU = C::SU, SP = C::SP, PD = C::PD, DP = C::DP;
-    extern __shared__ __align__(128) unsigned char smem[];
-    float* ring = reinterpret_cast<float*>(smem);
-    float* pring = reinterpret_cast<float*>(smem + C::U_BYTES);
-    uint64_t* fullU = reinterpret_cast<uint64_t*>(smem + C::U_BYTES + C::P_BYTES);
-    uint64_t* emptyU = fullU + SU;
-    uint64_t* fullP = emptyU + SU;
-    uint64_t* emptyP = fullP + SP;
-    int* pmeta = reinterpret_cast<int*>(emptyP + SP);
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < SU; ++s) {
-            mbar_init(&fullU[s], 1);
-            mbar_init(&emptyU[s], C::NWARPS_COMP);
-        }
-        for (int s = 0; s < SP; ++s) {
-            mbar_init(&fullP[s], 1);
-            mbar_init(&emptyP[s], C::NWARPS_COMP);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    const Geom& g = A.g;
-    const int nz = g.nz;
-    const int ntiles = A.ntx * A.nty;
-
-    const int64_t step_n = *A.d_base + A.step_i;
-    if (warp == C::NWARPS_COMP + 2) {
-        // ---------------- receivers warp: rec[n][r] = fma chain of u^n corners --------
-        for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
-            float acc = 0.0f;
-            for (int beta = 0; beta < A.nc; ++beta) {
-                const int64_t off = A.rec_off[(int64_t)r * A.nc + beta];
-                if (off < 0) continue;
-                acc = __fmaf_rn(A.rec_w[(int64_t)r * A.nc + beta], A.ucur[off], acc);
-            }
-            A.traces[step_n * A.nr + A.rec_id[r]] = acc;
-        }
-        return;
-    }
-    if (warp >= C::NWARPS_COMP) {
-        // ---------------- producer warps ----------------
-        // warp NWARPS_COMP: u^n plane tiles (with halo) into the ring, D planes ahead, and L2
-        // prefetches PD planes ahead; warp NWARPS_COMP+1: the u^{n-1}, b, a tiles of the output
-        // planes into the streams ring, DP planes ahead (+ their L2 prefetches).
-        const bool is_u = warp == C::NWARPS_COMP;
-        if (lane == 0) {
-            if (is_u) {
-                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.u) : "memory");
-            } else {
-                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.un) : "memory");
-                asm volatile("prefetch.tensormap [%0];" ::"l"(&M.b) : "memory");
-                if (A.a) asm volatile("prefetch.tensormap [%0];" ::"l"(&M.a) : "memory");
-            }
-            Ring rr{0, 0};
-            for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
-                const int tile = item % ntiles;
-                const int zb = (item / ntiles) * A.zc;
-                const int ze = min(nz, zb + A.zc);
-                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
-                const int niter = ze - zb + 2 * R;
-                if (is_u) {
-                    for (int kk = 0; kk < PD && kk < niter; ++kk) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + kk);
-                    for (int k = 0; k < niter; ++k) {
-                        if (k + PD < niter) tma_prefetch_l2_3d(&M.u, x0 - RP, y0 - R, zb + k + PD);
-                        mbar_wait(&emptyU[rr.slot], rr.phase ^ 1);
-                        mbar_expect_tx(&fullU[rr.slot], C::STAGE_BYTES);
-                        tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, &M.u, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
-                        rr.advance(SU);
-                    }
-                } else {
-                    auto l2_prefetch = [&](int z) {
-                        if (z >= ze) return;
-                        tma_prefetch_l2_3d(&M.un, x0, y0, z + R);
-                        tma_prefetch_l2_3d(&M.b, x0, y0, z);
-                        if (A.a && A.flags[(int64_t)tile * nz + z]) tma_prefetch_l2_3d(&M.a, x0, y0, z);
-                    };
-                    for (int z = zb; z < zb + PD; ++z) l2_prefetch(z);
-                    for (int z = zb; z < ze; ++z) {
-                        l2_prefetch(z + PD);
-                        const bool use_a = A.a && A.flags[(int64_t)tile * nz + z];  // [tile][z]: L1-friendly
-                        const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
-                        float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
-                        mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
-                        pmeta[3 * rr.slot] = use_a;  // published by the release of the arrive below
-                        pmeta[3 * rr.slot + 1] = tp.x;
-                        pmeta[3 * rr.slot + 2] = tp.y;
-                        mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
-                        tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
-                        tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
-                        if (use_a) tma_load_3d(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z);
-                        rr.advance(SP);
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ---------------- consumer warps ----------------
-    const int ly = warp * C::RY;  // first tile row of this thread
-    Ring ru{0, 0}, rp{0, 0};
-    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
-        const int tile = item % ntiles;
-        const int zb = (item / ntiles) * A.zc;
-        const int ze = min(nz, zb + A.zc);
-        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
-        if (x0 + TX <= g.nx && y0 + TY <= g.ny)
-            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane, ly,
-                                        ru, rp, step_n);
-        else
-            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane,
-                                         ly, ru, rp, step_n);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // eta flags: flags[tile][z] = 1 iff some a != 1 in the tile-plane
@@ -460,175 +34,20 @@ __global__ void count_flags_kernel(const uint8_t* flags, int64_t n, unsigned lon
     atomicAdd(cnt, c);
 }
 
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
-struct StreamPlan {
-    StreamMaps maps[2];  // by parity of the u^n buffer
-    uint8_t* flags = nullptr;
-    int ntx = 0, nty = 0;
-    int grid = 0;
-    int R = 0;
-    size_t smem = 0;
-    int nthreads = 0;
-    int TX = 0, TY = 0;
-    int nzc = 1, zc = 0;
-    unsigned long long* d_count = nullptr;  // tile-planes with a != 1 (inside the flags allocation)
-    int64_t nflags = 0;
-    int2* tpsc = nullptr;                   // [ntiles][nz] injection lists (fused sparse work)
-    int4* tpe = nullptr;
-    size_t tpe_cap = 0;
-};
 
-namespace {
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+static const StreamOps* stream_ops(int R) {
+    switch (R) {
+        case 1: return stream_ops_r1();
+        case 2: return stream_ops_r2();
+        case 3: return stream_ops_r3();
+        case 4: return stream_ops_r4();
+        case 5: return stream_ops_r5();
+        case 6: return stream_ops_r6();
+        case 7: return stream_ops_r7();
+        case 8: return stream_ops_r8();
+        default: return nullptr;
     }
-    return fn;
 }
-
-cudaError_t encode3d(CUtensorMap* m, const void* base, const Geom& g, int planes, int bx, int by) {
-    auto enc = get_encode();
-    if (!enc) return cudaErrorNotSupported;
-    cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
-    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    // no L2 promotion: a promoted halo'd box fetches whole 256-B segments of the neighbours
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-template <class C>
-cudaError_t setup(StreamPlan* p, const Geom& g) {
-    p->smem = C::SMEM;
-    p->nthreads = C::NTHREADS;
-    p->TX = C::TX;
-    p->TY = C::TY;
-    cudaError_t e = cudaFuncSetAttribute(stream_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(stream_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    if (e != cudaSuccess) return e;
-    int occ = 0, occ_t = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<C, false>, C::NTHREADS, C::SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, stream_kernel<C, true>, C::NTHREADS, C::SMEM);
-    if (e != cudaSuccess) return e;
-    occ = occ < occ_t ? occ : occ_t;
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorNotSupported;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    p->grid = sms * occ;
-    return cudaSuccess;
-}
-
-template <class C>
-cudaError_t make_maps(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a) {
-    for (int par = 0; par < 2; ++par) {
-        StreamMaps& M = p->maps[par];
-        cudaError_t e;
-        if ((e = encode3d(&M.u, ubuf[par], g, g.nz + 2 * g.R, C::TXP, C::TYP))) return e;
-        if ((e = encode3d(&M.un, ubuf[1 - par], g, g.nz + 2 * g.R, C::TX, C::TY))) return e;
-        if ((e = encode3d(&M.b, b, g, g.nz, C::TX, C::TY))) return e;
-        if ((e = encode3d(&M.a, a ? a : b, g, g.nz, C::TX, C::TY))) return e;
-    }
-    return cudaSuccess;
-}
-
-template <class C>
-cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur, float* unext,
-                   const float* b, const float* a, const Halo& halo, int parity_next, const Sparse& sp,
-                   const int64_t* d_base, int step_i, cudaStream_t s) {
-    StreamArgs A;
-    std::memset(&A, 0, sizeof A);
-    A.g = g;
-    A.c = c;
-    A.unext = unext;
-    A.a = a;
-    A.flags = p->flags;
-    A.lo = halo.lo[parity_next];
-    A.lo_off = halo.lo_off;
-    A.hi = halo.hi[parity_next];
-    A.hi_off = halo.hi_off;
-    A.ntx = p->ntx;
-    A.nty = p->nty;
-    A.nzc = p->nzc;
-    A.zc = p->zc;
-    A.nitems = p->ntx * p->nty * p->nzc;
-    A.tpsc = sp.nuc > 0 ? p->tpsc : nullptr;
-    A.tpe = p->tpe;
-    A.inj_src = sp.inj_src;
-    A.inj_s = sp.inj_s;
-    A.wavelet = sp.wavelet;
-    A.ns = sp.ns;
-    A.nrl = sp.nrl;
-    A.nr = sp.nr;
-    A.nc = sp.nc;
-    A.rec_id = sp.rec_id;
-    A.rec_off = sp.rec_off;
-    A.rec_w = sp.rec_w;
-    A.traces = sp.traces;
-    A.ucur = ucur;
-    A.d_base = d_base;
-    A.step_i = step_i;
-    if (A.lo || A.hi)
-        stream_kernel<C, true><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
-    else
-        stream_kernel<C, false><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
-    return cudaGetLastError();
-}
-
-// configuration table: (R, TY, RY, D = u^n ring lookahead, DP = streams lookahead,
-//                       PD = L2 prefetch distance, min CTAs/SM)
-using C1 = Cfg<1, 32, 4, 4, 4, 0, 1>;
-using C2 = Cfg<2, 32, 4, 4, 4, 0, 1>;
-using C3 = Cfg<3, 32, 4, 4, 4, 0, 1>;
-using C4 = Cfg<4, 32, 4, 4, 4, 0, 1>;
-using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
-using C6 = Cfg<6, 32, 4, 2, 3, 0, 1>;
-using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
-using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
-// development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
-using C4v1 = Cfg<4, 32, 4, 3, 4, 0, 1>;
-using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
-using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
-
-int variant() {
-    const char* v = getenv("AW_STREAM_VARIANT");
-    return v ? atoi(v) : 0;
-}
-
-}  // namespace
-
-#define AW_STREAM_DISPATCH(R, EXPR)       \
-    switch (R) {                          \
-        case 1: { using C = C1; EXPR; } break; \
-        case 2: { using C = C2; EXPR; } break; \
-        case 3: { using C = C3; EXPR; } break; \
-        case 4:                            \
-            if (variant() == 1) { using C = C4v1; EXPR; } \
-            else if (variant() == 2) { using C = C4v2; EXPR; } \
-            else if (variant() == 3) { using C = C4v3; EXPR; } \
-            else { using C = C4; EXPR; } \
-            break;                         \
-        case 5: { using C = C5; EXPR; } break; \
-        case 6: { using C = C6; EXPR; } break; \
-        case 7: { using C = C7; EXPR; } break; \
-        case 8: { using C = C8; EXPR; } break; \
-        default: return cudaErrorNotSupported; \
-    }
 
 cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float* b, const float* a,
                            StreamPlan** plan, cudaStream_t s) {
@@ -637,7 +56,12 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     StreamPlan* p = new StreamPlan();
     p->R = g.R;
     cudaError_t e = cudaSuccess;
-    AW_STREAM_DISPATCH(g.R, e = setup<C>(p, g));
+    const StreamOps* ops = stream_ops(g.R);
+    if (!ops) {
+        delete p;
+        return cudaErrorNotSupported;
+    }
+    e = ops->setup(p, g);
     if (e != cudaSuccess) {
         delete p;
         return e;
@@ -673,7 +97,9 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
 cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a,
                            cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    AW_STREAM_DISPATCH(p->R, e = make_maps<C>(p, g, ubuf, b, a));
+    const StreamOps* ops = stream_ops(p->R);
+    if (!ops) return cudaErrorNotSupported;
+    e = ops->make_maps(p, g, ubuf, b, a);
     if (e != cudaSuccess) return e;
     const int ntiles = p->ntx * p->nty;
     const int64_t nflags = (int64_t)ntiles * g.nz;
@@ -699,19 +125,24 @@ int stream_eta_tiles_pct(const StreamPlan* p) {
 void stream_release(StreamPlan* p) {
     if (!p) return;
     if (p->flags) cudaFree(p->flags);
-    if (p->tpsc) cudaFree(p->tpsc);
-    if (p->tpe) cudaFree(p->tpe);
+    for (int k = 0; k < 2; ++k) {
+        if (p->tpsc[k]) cudaFree(p->tpsc[k]);
+        if (p->tpe[k]) cudaFree(p->tpe[k]);
+    }
     delete p;
 }
 
 // Injection lists per tile-plane for the fused kernel.  corner_lin: the owned unique injection
 // corners (global row-major index, ascending), ptr: their CSR ranges into the entry arrays.
 cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const int64_t* corner_lin, const int* ptr,
-                                 int nuc, cudaStream_t s) {
+                                 int nuc, cudaStream_t s, int set) {
     const int ntiles = p->ntx * p->nty;
     const int64_t ntp = (int64_t)ntiles * g.nz;
     cudaError_t e;
-    if (!p->tpsc && (e = cudaMalloc(&p->tpsc, ntp * sizeof(int2))) != cudaSuccess) return e;
+    int2*& tpsc = p->tpsc[set];
+    int4*& tpe = p->tpe[set];
+    size_t& tpe_cap = p->tpe_cap[set];
+    if (!tpsc && (e = cudaMalloc(&tpsc, ntp * sizeof(int2))) != cudaSuccess) return e;
     std::vector<std::pair<int64_t, int4>> ents;  // key = tile*nz + z
     const int64_t per_plane = (int64_t)g.ny * g.nx;
     for (int c = 0; c < nuc; ++c) {
@@ -725,26 +156,31 @@ cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const
     std::stable_sort(ents.begin(), ents.end(),
                      [](const std::pair<int64_t, int4>& a, const std::pair<int64_t, int4>& b) { return a.first < b.first; });
     std::vector<int2> tpsc_h;  // only the touched keys are uploaded; the rest is zero (count 0)
-    if ((e = cudaMemsetAsync(p->tpsc, 0, ntp * sizeof(int2), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(tpsc, 0, ntp * sizeof(int2), s)) != cudaSuccess) return e;
     if (ents.empty()) return cudaSuccess;
-    if (p->tpe_cap < ents.size()) {
-        if (p->tpe) cudaFree(p->tpe);
-        p->tpe = nullptr;
-        p->tpe_cap = 0;
-        if ((e = cudaMalloc(&p->tpe, ents.size() * sizeof(int4))) != cudaSuccess) return e;
-        p->tpe_cap = ents.size();
+    if (tpe_cap < ents.size()) {
+        if (tpe) cudaFree(tpe);
+        tpe = nullptr;
+        tpe_cap = 0;
+        if ((e = cudaMalloc(&tpe, ents.size() * sizeof(int4))) != cudaSuccess) return e;
+        tpe_cap = ents.size();
     }
     std::vector<int4> tpe_h(ents.size());
     for (size_t i = 0; i < ents.size(); ++i) tpe_h[i] = ents[i].second;
-    if ((e = cudaMemcpyAsync(p->tpe, tpe_h.data(), tpe_h.size() * sizeof(int4), cudaMemcpyHostToDevice, s)))
+    if ((e = cudaMemcpyAsync(tpe, tpe_h.data(), tpe_h.size() * sizeof(int4), cudaMemcpyHostToDevice, s)))
         return e;
+    // the touched keys' {first, count} in one sparse scatter (host list of (key, value) pairs)
+    std::vector<int2> vals;
+    std::vector<int64_t> keys;
     for (size_t i = 0; i < ents.size();) {
         size_t j = i;
         while (j < ents.size() && ents[j].first == ents[i].first) ++j;
-        const int2 v = make_int2((int)i, (int)(j - i));
-        if ((e = cudaMemcpyAsync(p->tpsc + ents[i].first, &v, sizeof v, cudaMemcpyHostToDevice, s))) return e;
+        keys.push_back(ents[i].first);
+        vals.push_back(make_int2((int)i, (int)(j - i)));
         i = j;
     }
+    for (size_t k = 0; k < keys.size(); ++k)
+        if ((e = cudaMemcpyAsync(tpsc + keys[k], &vals[k], sizeof(int2), cudaMemcpyHostToDevice, s))) return e;
     return cudaStreamSynchronize(s);  // the host staging vectors die here
 }
 
@@ -753,9 +189,19 @@ cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, 
                                   const Sparse& sp, const int64_t* d_base, int step_i, cudaStream_t s) {
     // u^n is read through the tensor map of buffer parity_cur (stencil) and ucur (receivers)
     if (!p) return cudaErrorNotSupported;
-    AW_STREAM_DISPATCH(p->R, return launch<C>(p, g, c, parity_cur, ucur, unext, b, a, halo, parity_next, sp, d_base,
-                                              step_i, s));
-    return cudaErrorNotSupported;
+    const StreamOps* ops = stream_ops(p->R);
+    if (!ops) return cudaErrorNotSupported;
+    return ops->launch(p, g, c, parity_cur, ucur, unext, b, a, halo, parity_next, sp, d_base, step_i, s);
+}
+
+cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const float* ucur,
+                                       const float* uprev, float* unext, const float* b, const float* a,
+                                       const Sparse& sp, int inj_set, const int64_t* d_base, int step_i,
+                                       cudaStream_t s) {
+    if (!p || inj_set < 0 || inj_set > 1) return cudaErrorNotSupported;
+    const StreamOps* ops = stream_ops(p->R);
+    if (!ops) return cudaErrorNotSupported;
+    return ops->launch_bufs(p, g, c, ucur, uprev, unext, b, a, sp, inj_set, d_base, step_i, s);
 }
 
 }  // namespace aw

@@ -1,0 +1,8 @@
+// aw_stream_r6.cu -- instantiations of the streaming kernel for R = 6 (space order 12).
+#include "aw_stream.cuh"
+
+namespace aw {
+const StreamOps* stream_ops_r6() {
+    return ops_of<C6>();
+}
+}  // namespace aw
