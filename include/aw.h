@@ -74,7 +74,10 @@ enum {
     AW_OPT_TIMING = 2,      /* value 1: time every stencil launch with CUDA events (no graphs) */
     AW_OPT_GRAPH_STEPS = 3, /* value G >= 0: steps per captured CUDA graph (0 = no graphs) */
     AW_OPT_CHECK_FINITE = 4, /* value 0/1 (default 1): aw_run checks traces + final field */
-    AW_OPT_CHECKPOINT_STEPS = 5 /* value K >= 0: aw_fwi_gradient segment length (0 = auto, see there) */
+    AW_OPT_CHECKPOINT_STEPS = 5, /* value K >= 0: aw_fwi_gradient segment length (0 = auto, see there) */
+    AW_OPT_TEMPORAL = 6 /* value 0/1 (default 1): temporal blocking (NEXT-1) -- aw_run advances two steps per
+                           launch with the streaming kernel (3D, single slab; a third wavefield buffer is
+                           allocated); results are bit-identical to one step per launch */
 };
 
 /* multi-rank description: one process (or virtual rank) per slab of axis 0 */
@@ -192,6 +195,8 @@ typedef struct {
     int64_t launches_total; /* kernels launched by this handle since creation (all calls) */
     int64_t fwi_steps;    /* stencil steps of the last aw_fwi_gradient (forward + recompute + adjoint) */
     int fwi_checkpoint;   /* checkpoint segment length K used by the last aw_fwi_gradient */
+    int64_t timed_launches; /* stencil launches timed by the last aw_run (AW_OPT_TIMING; a temporal-
+                               blocking pass covers two of the n_stencil steps) */
 } aw_run_stats;
 
 aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out);

@@ -104,6 +104,14 @@ cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs
                                        const float* uprev, float* unext, const float* b, const float* a,
                                        const Sparse& sp, int inj_set, const int64_t* d_base, int step_i,
                                        cudaStream_t s);
+// NEXT-1 temporal blocking: one launch advances two steps (u^n = x, u^{n-1} = y) -> u^{n+1} in v
+// (a third buffer), u^{n+2} over y.  Single slab.  stream_tb_prepare sizes the completion array.
+cudaError_t stream_tb_prepare(StreamPlan* p, const Geom& g, int Z);
+cudaError_t launch_stencil_tb(StreamPlan* p, const Geom& g, const Coefs& c, const float* x, float* y, float* v,
+                              const float* b, const float* a, const Sparse& sp, const int64_t* d_base, int step_i,
+                              cudaStream_t s);
+// re-encode the per-parity maps after the caller permuted its wavefield buffers
+cudaError_t stream_remap(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a);
 
 // ---- NEXT-3 FWI kernels (aw_fwi.cu) ----
 // G += psi * D,  D = fl32(fl32(u1 - 2 u0) + um1), over the owned planes (wavefield layout inputs,

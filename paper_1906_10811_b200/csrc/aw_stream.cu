@@ -129,6 +129,7 @@ void stream_release(StreamPlan* p) {
         if (p->tpsc[k]) cudaFree(p->tpsc[k]);
         if (p->tpe[k]) cudaFree(p->tpe[k]);
     }
+    if (p->tb_done) cudaFree(p->tb_done);
     delete p;
 }
 
@@ -202,6 +203,46 @@ cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs
     const StreamOps* ops = stream_ops(p->R);
     if (!ops) return cudaErrorNotSupported;
     return ops->launch_bufs(p, g, c, ucur, uprev, unext, b, a, sp, inj_set, d_base, step_i, s);
+}
+
+// NEXT-1: temporal-blocking plan (completion-epoch array of the A items).  Z = planes per chunk,
+// >= 2R so a B chunk needs only the A chunks c-1 and c; 0 = default (16, or 2R if larger).
+cudaError_t stream_tb_prepare(StreamPlan* p, const Geom& g, int Z) {
+    if (!p) return cudaErrorNotSupported;
+    if (Z <= 0) Z = 16;
+    if (const char* z_env = getenv("AW_TB_Z")) {  // development knob
+        const int z = atoi(z_env);
+        if (z > 0) Z = z;
+    }
+    if (Z < 2 * g.R) Z = 2 * g.R;
+    const int nzc = (g.nz + Z - 1) / Z;
+    const int64_t n = (int64_t)nzc * p->ntx * p->nty;
+    if (p->tb_done && p->tb_Z == Z && p->tb_nzc == nzc) return cudaSuccess;
+    if (p->tb_done) cudaFree(p->tb_done);
+    p->tb_done = nullptr;
+    cudaError_t e = cudaMalloc(&p->tb_done, n * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    // epochs only grow, so the array is zeroed once (synchronously: no stream is involved yet)
+    if ((e = cudaMemset(p->tb_done, 0, n * sizeof(unsigned long long))) != cudaSuccess) return e;
+    p->tb_Z = Z;
+    p->tb_nzc = nzc;
+    p->tb_epoch = 0;
+    return cudaSuccess;
+}
+
+cudaError_t launch_stencil_tb(StreamPlan* p, const Geom& g, const Coefs& c, const float* x, float* y, float* v,
+                              const float* b, const float* a, const Sparse& sp, const int64_t* d_base, int step_i,
+                              cudaStream_t s) {
+    const StreamOps* ops = p ? stream_ops(p->R) : nullptr;
+    if (!ops) return cudaErrorNotSupported;
+    return ops->launch_tb(p, g, c, x, y, v, b, a, sp, d_base, step_i, s);
+}
+
+// Re-encode the per-parity tensor maps after the wavefield buffers were permuted (no kernels).
+cudaError_t stream_remap(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a) {
+    const StreamOps* ops = p ? stream_ops(p->R) : nullptr;
+    if (!ops) return cudaErrorNotSupported;
+    return ops->make_maps(p, g, ubuf, b, a);
 }
 
 }  // namespace aw

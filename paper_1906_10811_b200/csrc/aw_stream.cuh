@@ -189,7 +189,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                                              uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
                                              const volatile int* pmeta,
                                              int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
-                                             Ring& rp, int64_t step_n) {
+                                             Ring& rp, int64_t step_n, float* out_base) {
     constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
     const Geom& g = A.g;
     const int nz = g.nz;
@@ -208,7 +208,8 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
         ok_b[i] = inB && r;
     }
     // u^{n+1} of (z, y0+ly, xa): advanced by `plane` per output plane
-    float* outp = A.unext + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
+    // (out_base: A.unext, or the TB kernel's v / w buffer)
+    float* outp = out_base + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
 
     float2 q[RY][Q];
 #pragma unroll
@@ -292,7 +293,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                 }
                 if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
                     // fused exchange: boundary planes also go straight into the neighbour's halo
-                    const int64_t om = (outp - A.unext) - (int64_t)R * plane;  // model-layout index
+                    const int64_t om = (outp - out_base) - (int64_t)R * plane;  // model-layout index
                     float* h = (A.lo && z < R) ? A.lo + A.lo_off + om
                                                : A.hi + A.hi_off + om - (int64_t)(nz - R) * plane;
 #pragma unroll
@@ -436,10 +437,222 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
         if (x0 + TX <= g.nx && y0 + TY <= g.ny)
             consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane, ly,
-                                        ru, rp, step_n);
+                                        ru, rp, step_n, A.unext);
         else
             consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane,
-                                         ly, ru, rp, step_n);
+                                         ly, ru, rp, step_n, A.unext);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// NEXT-1: temporal blocking, two time steps per pass.
+//
+// A pass reads X = u^n (with halo), Y = u^{n-1}, b, a and writes V = u^{n+1} (a third
+// buffer) and W = u^{n+2} (over Y).  Work items are (tile, z-chunk) pairs of two kinds,
+// handed out in phase order A(0), B(0), A(1), B(1), ...:
+//   A(tile, c): step n   on planes [cZ+R, (c+1)Z+R) (A(0) from plane 0, the last to nz):
+//               the ordinary consumer with inputs (X, Y, b, a), output -> V, injection q[n];
+//   B(tile, c): step n+1 on planes [cZ, (c+1)Z): the same consumer with inputs
+//               (V with halo, X centre, b, a), output -> W (into Y), injection q[n+1].
+// B(tile, c) needs V on planes [cZ-R, (c+1)Z+R) of its tile and its four star neighbours,
+// i.e. the items A(., c-1) and A(., c), which come earlier in the hand-out order: the
+// u-producer waits on their completion epochs (acquire) before its TMA loads, so the pass
+// is deadlock-free for any grid shape (every CTA is resident and takes items in order).
+// The A phase of a chunk is ~Z planes of all tiles behind its B phase, so with Z planes of
+// every field fitting in L2 the second step reads V, X, b, a from L2: the HBM traffic of a
+// pass is X, Y, b, a once plus the V and W writes (~10.7 B per point update instead of 16).
+// Y is overwritten by B(tile, c) only after A(tile, c) -- the only reader of those planes
+// of Y -- finished (B waits for it).  Per point the arithmetic is the canonical sequence,
+// so two steps of this kernel equal two steps of stream_kernel bit for bit.
+// ---------------------------------------------------------------------------
+struct TbMaps {
+    CUtensorMap xh;  // X with halo box (TXP, TYP): A items' u^n ring
+    CUtensorMap vh;  // V with halo box: B items' u^n ring
+    CUtensorMap y;   // Y centre box (TX, TY): A items' u^{n-1}
+    CUtensorMap xc;  // X centre box: B items' u^{n-1}
+    CUtensorMap b;
+    CUtensorMap a;
+};
+
+struct TbArgs {
+    StreamArgs s;                  // geometry, coefficients, eta flags, injection lists, receivers (ucur = X)
+    float* v;                      // V base (plane -R)
+    float* w;                      // Y base: B items' output u^{n+2}
+    unsigned long long* done;      // [nzc][ntiles]: epoch at which A(tile, c) completed
+    unsigned long long epoch;      // this pass's epoch (monotone per plan)
+    int Z, nzc;
+};
+
+__device__ __forceinline__ void tb_decode(int item, int ntiles, int nzc, int Z, int R, int nz, int& tile, int& c,
+                                          bool& isB, int& zb, int& ze) {
+    const int phase = item / ntiles;
+    tile = item - phase * ntiles;
+    c = phase >> 1;
+    isB = phase & 1;
+    if (isB) {
+        zb = c * Z;
+        ze = min(nz, zb + Z);
+    } else {
+        zb = c == 0 ? 0 : c * Z + R;
+        ze = c == nzc - 1 ? nz : min(nz, (c + 1) * Z + R);
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_epoch(const unsigned long long* p, unsigned long long epoch) {
+    while (ld_acquire_u64(p) < epoch) __nanosleep(64);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
+    tb_kernel(const __grid_constant__ TbMaps M, const __grid_constant__ TbArgs T) {
+    constexpr int R = C::R, TX = C::TX, TY = C::TY, RP = C::RP, SU = C::SU, SP = C::SP;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);
+    float* pring = reinterpret_cast<float*>(smem + C::U_BYTES);
+    uint64_t* fullU = reinterpret_cast<uint64_t*>(smem + C::U_BYTES + C::P_BYTES);
+    uint64_t* emptyU = fullU + SU;
+    uint64_t* fullP = emptyU + SU;
+    uint64_t* emptyP = fullP + SP;
+    int* pmeta = reinterpret_cast<int*>(emptyP + SP);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < SU; ++s) {
+            mbar_init(&fullU[s], 1);
+            mbar_init(&emptyU[s], C::NWARPS_COMP);
+        }
+        for (int s = 0; s < SP; ++s) {
+            mbar_init(&fullP[s], 1);
+            mbar_init(&emptyP[s], C::NWARPS_COMP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const StreamArgs& A = T.s;
+    const Geom& g = A.g;
+    const int nz = g.nz;
+    const int ntiles = A.ntx * A.nty;
+    const int nitems = 2 * T.nzc * ntiles;
+    const int64_t step_n = *A.d_base + A.step_i;  // the pass advances steps n and n+1
+
+    if (warp == C::NWARPS_COMP + 2) {
+        // ---- receivers: rec[n] from X (read-only in this pass), rec[n+1] from V once the A items
+        // owning its corners completed (they never wait, so this cannot deadlock) ----
+        for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
+            float acc = 0.0f;
+            for (int beta = 0; beta < A.nc; ++beta) {
+                const int64_t off = A.rec_off[(int64_t)r * A.nc + beta];
+                if (off < 0) continue;
+                acc = __fmaf_rn(A.rec_w[(int64_t)r * A.nc + beta], A.ucur[off], acc);
+            }
+            A.traces[step_n * A.nr + A.rec_id[r]] = acc;
+            acc = 0.0f;
+            for (int beta = 0; beta < A.nc; ++beta) {
+                const int64_t off = A.rec_off[(int64_t)r * A.nc + beta];
+                if (off < 0) continue;
+                const int z = (int)(off / g.plane) - R;
+                const int rem = (int)(off - (int64_t)(z + R) * g.plane);
+                const int y = rem / (int)g.pitch, x = rem - y * (int)g.pitch;
+                const int tile = (y / TY) * A.ntx + x / TX;
+                const int c = z < T.Z + R ? 0 : min(T.nzc - 1, (z - R) / T.Z);
+                wait_epoch(T.done + (int64_t)c * ntiles + tile, T.epoch);
+                acc = __fmaf_rn(A.rec_w[(int64_t)r * A.nc + beta], __ldcg(T.v + off), acc);
+            }
+            A.traces[(step_n + 1) * A.nr + A.rec_id[r]] = acc;
+        }
+        return;
+    }
+    if (warp >= C::NWARPS_COMP) {
+        // ---- producers: as in stream_kernel, with the map pair chosen by the item kind ----
+        const bool is_u = warp == C::NWARPS_COMP;
+        if (lane == 0) {
+            Ring rr{0, 0};
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int tile, c, zb, ze;
+                bool isB;
+                tb_decode(item, ntiles, T.nzc, T.Z, R, nz, tile, c, isB, zb, ze);
+                if (zb >= ze) continue;
+                const int tx = tile % A.ntx, ty = tile / A.ntx;
+                const int x0 = tx * TX, y0 = ty * TY;
+                if (is_u) {
+                    if (isB) {
+                        // V of this tile and its star neighbours on chunks c-1, c must be complete
+                        const int nb[5] = {tile, tx > 0 ? tile - 1 : -1, tx + 1 < A.ntx ? tile + 1 : -1,
+                                           ty > 0 ? tile - A.ntx : -1, ty + 1 < A.nty ? tile + A.ntx : -1};
+                        for (int cc = c > 0 ? c - 1 : 0; cc <= c; ++cc)
+                            for (int q = 0; q < 5; ++q)
+                                if (nb[q] >= 0) wait_epoch(T.done + (int64_t)cc * ntiles + nb[q], T.epoch);
+                        // generic-proxy stores of other CTAs -> this CTA's async-proxy (TMA) reads
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    const CUtensorMap* mu = isB ? &M.vh : &M.xh;
+                    const int niter = ze - zb + 2 * R;
+                    for (int k = 0; k < niter; ++k) {
+                        mbar_wait(&emptyU[rr.slot], rr.phase ^ 1);
+                        mbar_expect_tx(&fullU[rr.slot], C::STAGE_BYTES);
+                        tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, mu, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
+                        rr.advance(SU);
+                    }
+                } else {
+                    const CUtensorMap* mp = isB ? &M.xc : &M.y;
+                    for (int z = zb; z < ze; ++z) {
+                        const bool use_a = A.a && A.flags[(int64_t)tile * nz + z];
+                        const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
+                        float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
+                        mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
+                        pmeta[3 * rr.slot] = use_a;
+                        pmeta[3 * rr.slot + 1] = tp.x;
+                        pmeta[3 * rr.slot + 2] = tp.y;
+                        mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
+                        tma_load_3d(dst, mp, &fullP[rr.slot], x0, y0, z + R);
+                        tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
+                        if (use_a) tma_load_3d(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z);
+                        rr.advance(SP);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    const int ly = warp * C::RY;
+    Ring ru{0, 0}, rp{0, 0};
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int tile, c, zb, ze;
+        bool isB;
+        tb_decode(item, ntiles, T.nzc, T.Z, R, nz, tile, c, isB, zb, ze);
+        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+        if (zb < ze) {
+            float* out = isB ? T.w : T.v;
+            const int64_t n_inj = step_n + (isB ? 1 : 0);
+            if (x0 + TX <= g.nx && y0 + TY <= g.ny)
+                consume_item<C, true, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
+                                             lane, ly, ru, rp, n_inj, out);
+            else
+                consume_item<C, false, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
+                                              y0, lane, ly, ru, rp, n_inj, out);
+        }
+        if (!isB) {
+            // publish "A(tile, c) complete": every consumer's V stores, then one release
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(C::NCOMP) : "memory");
+            if (tid == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(T.done + (int64_t)c * ntiles + tile),
+                             "l"(T.epoch)
+                             : "memory");
+            }
+        }
     }
 }
 
@@ -461,6 +674,10 @@ struct StreamPlan {
     int2* tpsc[2] = {nullptr, nullptr};     // [ntiles][nz] injection lists (fused sparse work), per set
     int4* tpe[2] = {nullptr, nullptr};      // set 0: sources; set 1: FWI adjoint sources (receivers)
     size_t tpe_cap[2] = {0, 0};
+    // NEXT-1 temporal blocking
+    unsigned long long* tb_done = nullptr;  // [tb_nzc][ntiles] completion epochs of the A items
+    unsigned long long tb_epoch = 0;        // last epoch handed out (monotone)
+    int tb_Z = 0, tb_nzc = 0;
 };
 
 namespace {
@@ -502,12 +719,18 @@ cudaError_t setup(StreamPlan* p, const Geom& g) {
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(stream_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tb_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
     int occ = 0, occ_t = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<C, false>, C::NTHREADS, C::SMEM);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, stream_kernel<C, true>, C::NTHREADS, C::SMEM);
     if (e != cudaSuccess) return e;
     occ = occ < occ_t ? occ : occ_t;
+    int occ_tb = 0;  // the temporal-blocking kernel shares the grid (all its CTAs must be resident)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tb, tb_kernel<C>, C::NTHREADS, C::SMEM);
+    if (e != cudaSuccess) return e;
+    occ = occ < occ_tb ? occ : occ_tb;
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorNotSupported;
     int dev = 0, sms = 0;
@@ -617,6 +840,55 @@ cudaError_t launch_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const floa
     return cudaGetLastError();
 }
 
+// One two-step pass of the temporal-blocking kernel (single slab).
+template <class C>
+cudaError_t launch_tb(StreamPlan* p, const Geom& g, const Coefs& c, const float* x, float* y, float* v,
+                      const float* b, const float* a, const Sparse& sp, const int64_t* d_base, int step_i,
+                      cudaStream_t s) {
+    if (!p->tb_done) return cudaErrorNotSupported;
+    TbMaps M;
+    cudaError_t e;
+    if ((e = encode3d(&M.xh, x, g, g.nz + 2 * g.R, C::TXP, C::TYP))) return e;
+    if ((e = encode3d(&M.vh, v, g, g.nz + 2 * g.R, C::TXP, C::TYP))) return e;
+    if ((e = encode3d(&M.y, y, g, g.nz + 2 * g.R, C::TX, C::TY))) return e;
+    if ((e = encode3d(&M.xc, x, g, g.nz + 2 * g.R, C::TX, C::TY))) return e;
+    if ((e = encode3d(&M.b, b, g, g.nz, C::TX, C::TY))) return e;
+    if ((e = encode3d(&M.a, a ? a : b, g, g.nz, C::TX, C::TY))) return e;
+    TbArgs T;
+    std::memset(&T, 0, sizeof T);
+    StreamArgs& A = T.s;
+    A.g = g;
+    A.c = c;
+    A.a = a;
+    A.flags = p->flags;
+    A.ntx = p->ntx;
+    A.nty = p->nty;
+    A.tpsc = sp.nuc > 0 ? p->tpsc[0] : nullptr;
+    A.tpe = p->tpe[0];
+    A.inj_src = sp.inj_src;
+    A.inj_s = sp.inj_s;
+    A.wavelet = sp.wavelet;
+    A.ns = sp.ns;
+    A.nrl = sp.nrl;
+    A.nr = sp.nr;
+    A.nc = sp.nc;
+    A.rec_id = sp.rec_id;
+    A.rec_off = sp.rec_off;
+    A.rec_w = sp.rec_w;
+    A.traces = sp.traces;
+    A.ucur = x;
+    A.d_base = d_base;
+    A.step_i = step_i;
+    T.v = v;
+    T.w = y;
+    T.done = p->tb_done;
+    T.epoch = ++p->tb_epoch;
+    T.Z = p->tb_Z;
+    T.nzc = p->tb_nzc;
+    tb_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, T);
+    return cudaGetLastError();
+}
+
 // configuration table: (R, TY, RY, D = u^n ring lookahead, DP = streams lookahead,
 //                       PD = L2 prefetch distance, min CTAs/SM)
 using C1 = Cfg<1, 32, 4, 4, 4, 0, 1>;
@@ -647,6 +919,8 @@ struct StreamOps {
                           const float*, const Halo&, int, const Sparse&, const int64_t*, int, cudaStream_t);
     cudaError_t (*launch_bufs)(StreamPlan*, const Geom&, const Coefs&, const float*, const float*, float*,
                                const float*, const float*, const Sparse&, int, const int64_t*, int, cudaStream_t);
+    cudaError_t (*launch_tb)(StreamPlan*, const Geom&, const Coefs&, const float*, float*, float*, const float*,
+                             const float*, const Sparse&, const int64_t*, int, cudaStream_t);
 };
 const StreamOps* stream_ops_r1();
 const StreamOps* stream_ops_r2();
@@ -660,7 +934,7 @@ const StreamOps* stream_ops_r8();
 namespace {
 template <class C>
 const StreamOps* ops_of() {
-    static const StreamOps o{setup<C>, make_maps<C>, launch<C>, launch_bufs<C>};
+    static const StreamOps o{setup<C>, make_maps<C>, launch<C>, launch_bufs<C>, launch_tb<C>};
     return &o;
 }
 }  // namespace
