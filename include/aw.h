@@ -75,9 +75,13 @@ enum {
     AW_OPT_GRAPH_STEPS = 3, /* value G >= 0: steps per captured CUDA graph (0 = no graphs) */
     AW_OPT_CHECK_FINITE = 4, /* value 0/1 (default 1): aw_run checks traces + final field */
     AW_OPT_CHECKPOINT_STEPS = 5, /* value K >= 0: aw_fwi_gradient segment length (0 = auto, see there) */
-    AW_OPT_TEMPORAL = 6 /* value 0/1 (default 1): temporal blocking (NEXT-1) -- aw_run advances two steps per
+    AW_OPT_TEMPORAL = 6, /* value 0/1 (default 0): temporal blocking (NEXT-1) -- aw_run advances two steps per
                            launch with the streaming kernel (3D, single slab; a third wavefield buffer is
-                           allocated); results are bit-identical to one step per launch */
+                           allocated); results are bit-identical to one step per launch.  Off by default:
+                           measured 6-45 % slower than one step per launch on B200 (NEXT-1) */
+    AW_OPT_FWI_ACCUMULATE = 7 /* value 0/1 (default 0): NEXT-4 multi-shot -- with 1, aw_fwi_gradient writes the
+                           fp32 sum (in call order) of the gradients of all calls since the option was last
+                           set; setting it (either value) clears the sum.  J is still per call. */
 };
 
 /* multi-rank description: one process (or virtual rank) per slab of axis 0 */

@@ -203,8 +203,11 @@ struct aw_grid {
     float* fwi_pool = nullptr;             // nbuf wavefield-sized buffers
     int64_t fwi_pool_nbuf = 0;
     int opt_ckpt = 0;                      // AW_OPT_CHECKPOINT_STEPS (0 = auto)
+    int opt_accum = 0;                     // AW_OPT_FWI_ACCUMULATE
+    bool acc_valid = false;                // d_Gacc holds the sum of the gradients since the option was set
+    float* d_Gacc = nullptr;
     // NEXT-1 temporal blocking (two steps per launch): third wavefield buffer, readiness
-    int opt_temporal = 1;                  // AW_OPT_TEMPORAL
+    int opt_temporal = 0;                  // AW_OPT_TEMPORAL (off: measured slower on B200, DESIGN.md NEXT-1)
     float* ubuf_spare = nullptr;
     bool tb_ready = false;
     int n_timed = 0;                       // timed stencil launches of the last run (AW_OPT_TIMING)
@@ -987,6 +990,7 @@ void aw_grid_destroy(aw_grid* g) {
     dfree(g->adj_arena);
     dfree(g->fwi_arena);
     dfree(g->fwi_pool);
+    dfree(g->d_Gacc);
     dfree(g->ubuf[0]);
     dfree(g->ubuf[1]);
     dfree(g->ubuf_spare);
@@ -1359,11 +1363,23 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     // ---- 4. gradient = -G / dt^2, outputs ----
     CK(aw::launch_fwi_finalize(g->geom, d_G, dt, g->s));
     ++launches;
+    const float* g_out = d_G;
+    if (g->opt_accum) {  // NEXT-4: sum of the gradients of the calls since AW_OPT_FWI_ACCUMULATE was set
+        if (!g->d_Gacc) CK(cudaMalloc((void**)&g->d_Gacc, g->mbytes));
+        if (g->acc_valid) {
+            CK(aw::launch_fwi_accumulate(g->geom, g->d_Gacc, d_G, g->s));
+            ++launches;
+        } else {
+            CK(cudaMemcpyAsync(g->d_Gacc, d_G, g->mbytes, cudaMemcpyDeviceToDevice, g->s));
+        }
+        g->acc_valid = true;
+        g_out = g->d_Gacc;
+    }
     CK(cudaEventRecord(g->ev_t1, g->s));
     {
         const int64_t nx = g->geom.nx, ny = g->geom.ny;
         float* dst = layout == AW_GLOBAL ? grad + g->z0 * ny * nx : grad;
-        if ((st = copy_out(g, dst, d_G, g->geom.pitch, nx, (int64_t)g->geom.nz * ny))) return st;
+        if ((st = copy_out(g, dst, g_out, g->geom.pitch, nx, (int64_t)g->geom.nz * ny))) return st;
     }
     if (residual)
         CK(cudaMemcpyAsync(residual, d_res, tr, ptr_kind(residual) == PK_DEVICE ? cudaMemcpyDeviceToDevice
@@ -1504,6 +1520,11 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
             g->opt_temporal = (int)value;
             g->coeffs_valid = false;  // re-prepare (allocates the third buffer when enabled)
             free_graphs(g);
+            return AW_OK;
+        case AW_OPT_FWI_ACCUMULATE:
+            if (value < 0 || value > 1) return fail(AW_EINVAL, "accumulate option must be 0 or 1");
+            g->opt_accum = (int)value;
+            g->acc_valid = false;  // setting the option (either value) clears the sum
             return AW_OK;
         case AW_OPT_CHECKPOINT_STEPS:
             if (value < 0 || value > (1 << 30)) return fail(AW_EINVAL, "checkpoint steps out of range");

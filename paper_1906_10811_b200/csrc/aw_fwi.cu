@@ -92,4 +92,24 @@ cudaError_t launch_fwi_finalize(const Geom& g, float* G, double dt, cudaStream_t
     return cudaGetLastError();
 }
 
+// NEXT-4 multi-shot: acc = fl32(acc + grad), the per-shot gradients summed in call order
+__global__ void fwi_accumulate_kernel(float4* __restrict__ acc, const float4* __restrict__ G, int64_t n4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = acc[i];
+        const float4 g = G[i];
+        a.x = __fadd_rn(a.x, g.x);
+        a.y = __fadd_rn(a.y, g.y);
+        a.z = __fadd_rn(a.z, g.z);
+        a.w = __fadd_rn(a.w, g.w);
+        acc[i] = a;
+    }
+}
+
+cudaError_t launch_fwi_accumulate(const Geom& g, float* acc, const float* G, cudaStream_t s) {
+    const int64_t n4 = (int64_t)g.nz * g.plane / 4;
+    fwi_accumulate_kernel<<<stream_blocks(n4), 256, 0, s>>>(reinterpret_cast<float4*>(acc),
+                                                             reinterpret_cast<const float4*>(G), n4);
+    return cudaGetLastError();
+}
+
 }  // namespace aw

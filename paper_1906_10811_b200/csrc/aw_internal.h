@@ -123,5 +123,7 @@ cudaError_t launch_fwi_residual(const float* rec, const float* dobs, float* res,
                                 double* J, cudaStream_t s);
 // grad = fl32(-(double)G / dt^2) in place (model layout, padding stays 0)
 cudaError_t launch_fwi_finalize(const Geom& g, float* G, double dt, cudaStream_t s);
+// acc = fl32(acc + G) (model layout; NEXT-4 multi-shot gradient sums)
+cudaError_t launch_fwi_accumulate(const Geom& g, float* acc, const float* G, cudaStream_t s);
 
 }  // namespace aw

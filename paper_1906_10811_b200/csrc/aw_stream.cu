@@ -209,12 +209,15 @@ cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs
 // >= 2R so a B chunk needs only the A chunks c-1 and c; 0 = default (16, or 2R if larger).
 cudaError_t stream_tb_prepare(StreamPlan* p, const Geom& g, int Z) {
     if (!p) return cudaErrorNotSupported;
-    if (Z <= 0) Z = 16;
+    if (Z <= 0) Z = 32;  // best of 8/16/24/32/48/64 on C3 (profiles/r1/tb_sweep.jsonl)
     if (const char* z_env = getenv("AW_TB_Z")) {  // development knob
         const int z = atoi(z_env);
         if (z > 0) Z = z;
     }
     if (Z < 2 * g.R) Z = 2 * g.R;
+    int lead = 2;  // A phases handed out ahead of the first B phase (>= 1: B(c) must follow A(c))
+    if (const char* l_env = getenv("AW_TB_LEAD")) lead = atoi(l_env) > 1 ? atoi(l_env) : 1;
+    p->tb_lead = lead;
     const int nzc = (g.nz + Z - 1) / Z;
     const int64_t n = (int64_t)nzc * p->ntx * p->nty;
     if (p->tb_done && p->tb_Z == Z && p->tb_nzc == nzc) return cudaSuccess;

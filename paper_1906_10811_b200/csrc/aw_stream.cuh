@@ -83,6 +83,30 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA load with an L2 cache-eviction policy (createpolicy): temporal blocking keeps the data the
+// second step re-reads (evict_last) and lets the single-use streams go first (evict_first)
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(policy) : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
                  "r"(c2)
@@ -189,7 +213,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                                              uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
                                              const volatile int* pmeta,
                                              int tile, int zb, int ze, int x0, int y0, int lane, int ly, Ring& ru,
-                                             Ring& rp, int64_t step_n, float* out_base) {
+                                             Ring& rp, int64_t step_n, float* out_base, uint64_t st_policy = 0) {
     constexpr int R = C::R, RY = C::RY, RP = C::RP, TXP = C::TXP, TX = C::TX, SU = C::SU, SP = C::SP, Q = C::Q;
     const Geom& g = A.g;
     const int nz = g.nz;
@@ -285,11 +309,20 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                         if (xl < 32) res[i].x = v; else res[i].y = v;
                     }
                 }
+                if (st_policy) {
 #pragma unroll
-                for (int i = 0; i < RY; ++i) {
-                    float* o = outp + i * pitch;
-                    if (ok_a[i]) o[0] = res[i].x;
-                    if (ok_b[i]) o[32] = res[i].y;
+                    for (int i = 0; i < RY; ++i) {
+                        float* o = outp + i * pitch;
+                        if (ok_a[i]) st_hint(o, res[i].x, st_policy);
+                        if (ok_b[i]) st_hint(o + 32, res[i].y, st_policy);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) {
+                        float* o = outp + i * pitch;
+                        if (ok_a[i]) o[0] = res[i].x;
+                        if (ok_b[i]) o[32] = res[i].y;
+                    }
                 }
                 if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
                     // fused exchange: boundary planes also go straight into the neighbour's halo
@@ -481,15 +514,28 @@ struct TbArgs {
     float* w;                      // Y base: B items' output u^{n+2}
     unsigned long long* done;      // [nzc][ntiles]: epoch at which A(tile, c) completed
     unsigned long long epoch;      // this pass's epoch (monotone per plan)
-    int Z, nzc;
+    int Z, nzc, lead;              // chunk planes, chunks, A phases handed out ahead of B(0)
 };
 
-__device__ __forceinline__ void tb_decode(int item, int ntiles, int nzc, int Z, int R, int nz, int& tile, int& c,
-                                          bool& isB, int& zb, int& ze) {
+// Phase order with lead L >= 1: A(0) .. A(L-1), then B(0), A(L), B(1), A(L+1), ... (2 nzc + L phases;
+// the A phases past the last chunk are empty: c = nzc marks a no-op item).
+__device__ __forceinline__ void tb_decode(int item, int ntiles, int nzc, int Z, int R, int nz, int lead, int& tile,
+                                          int& c, bool& isB, int& zb, int& ze) {
     const int phase = item / ntiles;
     tile = item - phase * ntiles;
-    c = phase >> 1;
-    isB = phase & 1;
+    if (phase < lead) {
+        c = phase;
+        isB = false;
+    } else {
+        const int r = phase - lead;
+        isB = !(r & 1);
+        c = isB ? r >> 1 : lead + (r >> 1);
+    }
+    if (c >= nzc) {
+        zb = ze = 0;
+        c = nzc;
+        return;
+    }
     if (isB) {
         zb = c * Z;
         ze = min(nz, zb + Z);
@@ -541,7 +587,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const Geom& g = A.g;
     const int nz = g.nz;
     const int ntiles = A.ntx * A.nty;
-    const int nitems = 2 * T.nzc * ntiles;
+    const int nitems = (2 * T.nzc + T.lead) * ntiles;
     const int64_t step_n = *A.d_base + A.step_i;  // the pass advances steps n and n+1
 
     if (warp == C::NWARPS_COMP + 2) {
@@ -575,11 +621,12 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         // ---- producers: as in stream_kernel, with the map pair chosen by the item kind ----
         const bool is_u = warp == C::NWARPS_COMP;
         if (lane == 0) {
+            const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
             Ring rr{0, 0};
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
                 int tile, c, zb, ze;
                 bool isB;
-                tb_decode(item, ntiles, T.nzc, T.Z, R, nz, tile, c, isB, zb, ze);
+                tb_decode(item, ntiles, T.nzc, T.Z, R, nz, T.lead, tile, c, isB, zb, ze);
                 if (zb >= ze) continue;
                 const int tx = tile % A.ntx, ty = tile / A.ntx;
                 const int x0 = tx * TX, y0 = ty * TY;
@@ -599,7 +646,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                     for (int k = 0; k < niter; ++k) {
                         mbar_wait(&emptyU[rr.slot], rr.phase ^ 1);
                         mbar_expect_tx(&fullU[rr.slot], C::STAGE_BYTES);
-                        tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, mu, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
+                        if (isB)  // V: last readers are this item and its neighbours, soon -- default policy
+                            tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, mu, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
+                        else      // X: the B items re-read it as u^{n-1}
+                            tma_load_3d_hint(ring + rr.slot * C::STAGE_STRIDE_F, mu, &fullU[rr.slot], x0 - RP, y0 - R,
+                                             zb + k, keep);
                         rr.advance(SU);
                     }
                 } else {
@@ -613,9 +664,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         pmeta[3 * rr.slot + 1] = tp.x;
                         pmeta[3 * rr.slot + 2] = tp.y;
                         mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
-                        tma_load_3d(dst, mp, &fullP[rr.slot], x0, y0, z + R);
-                        tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
-                        if (use_a) tma_load_3d(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z);
+                        // A: Y is dead after this read, b and a are re-read by B; B: last use of all three
+                        const uint64_t pb = isB ? drop : keep;
+                        tma_load_3d_hint(dst, mp, &fullP[rr.slot], x0, y0, z + R, drop);
+                        tma_load_3d_hint(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z, pb);
+                        if (use_a) tma_load_3d_hint(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z, pb);
                         rr.advance(SP);
                     }
                 }
@@ -626,23 +679,25 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 
     // ---- consumers ----
     const int ly = warp * C::RY;
+    const uint64_t st_keep = policy_evict_last(), st_drop = policy_evict_first();
     Ring ru{0, 0}, rp{0, 0};
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
         int tile, c, zb, ze;
         bool isB;
-        tb_decode(item, ntiles, T.nzc, T.Z, R, nz, tile, c, isB, zb, ze);
+        tb_decode(item, ntiles, T.nzc, T.Z, R, nz, T.lead, tile, c, isB, zb, ze);
         const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
         if (zb < ze) {
             float* out = isB ? T.w : T.v;
             const int64_t n_inj = step_n + (isB ? 1 : 0);
+            const uint64_t pol = isB ? st_drop : st_keep;  // V is re-read by B; W only by the next pass
             if (x0 + TX <= g.nx && y0 + TY <= g.ny)
                 consume_item<C, true, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
-                                             lane, ly, ru, rp, n_inj, out);
+                                             lane, ly, ru, rp, n_inj, out, pol);
             else
                 consume_item<C, false, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
-                                              y0, lane, ly, ru, rp, n_inj, out);
+                                              y0, lane, ly, ru, rp, n_inj, out, pol);
         }
-        if (!isB) {
+        if (!isB && c < T.nzc) {
             // publish "A(tile, c) complete": every consumer's V stores, then one release
             asm volatile("fence.proxy.async.global;" ::: "memory");
             asm volatile("bar.sync 1, %0;" ::"r"(C::NCOMP) : "memory");
@@ -677,7 +732,7 @@ struct StreamPlan {
     // NEXT-1 temporal blocking
     unsigned long long* tb_done = nullptr;  // [tb_nzc][ntiles] completion epochs of the A items
     unsigned long long tb_epoch = 0;        // last epoch handed out (monotone)
-    int tb_Z = 0, tb_nzc = 0;
+    int tb_Z = 0, tb_nzc = 0, tb_lead = 1;
 };
 
 namespace {
@@ -885,6 +940,7 @@ cudaError_t launch_tb(StreamPlan* p, const Geom& g, const Coefs& c, const float*
     T.epoch = ++p->tb_epoch;
     T.Z = p->tb_Z;
     T.nzc = p->tb_nzc;
+    T.lead = p->tb_lead;
     tb_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, T);
     return cudaGetLastError();
 }

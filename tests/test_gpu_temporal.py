@@ -96,6 +96,7 @@ def test_temporal_then_other_paths(aw):
     """After TB runs permuted the buffers: set_wavefield, graphs (TB off), TB again, FWI gradient."""
     w = workloads.small_case((33, 40, 70), 4, 20, nbl=3, ns=2, nr=5, seed=9)
     g = aw.Grid(w.shape, w.extent, 4)
+    g.set_option(aw.AW_OPT_TEMPORAL, 1)
     g.set_model(w.m, w.damp)
     g.add_sources(w.src_coords, w.wavelet)
     g.add_receivers(w.rec_coords, 20)
