@@ -124,9 +124,14 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
-template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_>
+template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_, bool ADJ_ = true>
 struct Cfg {
     static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
+    // lane -> columns: ADJ = the adjacent pair (2l, 2l+1), read and written with 64-bit shared/global
+    // accesses; otherwise (l, l+32) with 32-bit accesses (the round-1 mapping, kept for A/B runs)
+    static constexpr bool ADJ = ADJ_;
+    static constexpr int CA = ADJ ? 2 : 1;   // first column = CA * lane
+    static constexpr int CB = ADJ ? 1 : 32;  // second column = first + CB
     static constexpr int Q = 2 * R + 1;  // z queue length (and plane-loop unroll)
     // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
     // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
@@ -222,7 +227,13 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
     const int64_t pitch = g.pitch, plane = g.plane;
     const float2 C0 = f2(A.c.C0, A.c.C0);
     const float2 two = f2(2.0f, 2.0f), one = f2(1.0f, 1.0f);
-    const int xa = x0 + lane, xb = x0 + lane + 32;
+    constexpr int CA = C::CA, CB = C::CB;
+    // both columns of this lane as one float2 (64-bit load when ADJ)
+    auto ld2 = [](const float* p) -> float2 {
+        if constexpr (C::ADJ) return *reinterpret_cast<const float2*>(p);
+        else return f2(p[0], p[CB]);
+    };
+    const int xa = x0 + CA * lane, xb = xa + CB;
     const bool inA = INTERIOR || xa < g.nx, inB = INTERIOR || xb < g.nx;
     bool ok_a[RY], ok_b[RY];
 #pragma unroll
@@ -233,7 +244,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
     }
     // u^{n+1} of (z, y0+ly, xa): advanced by `plane` per output plane
     // (out_base: A.unext, or the TB kernel's v / w buffer)
-    float* outp = out_base + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;
+    float* outp = out_base + (int64_t)(zb + R) * plane + (int64_t)(y0 + ly) * pitch + xa;  // (xb = xa + CB)
 
     float2 q[RY][Q];
 #pragma unroll
@@ -247,34 +258,50 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
             const int k = kb + uq;
             if (k >= niter) break;
             mbar_wait(&fullU[ru.slot], ru.phase);
-            const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + lane;
+            const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + CA * lane;
             // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
 #pragma unroll
-            for (int i = 0; i < RY; ++i) q[i][uq] = f2(P[i * TXP], P[i * TXP + 32]);
+            for (int i = 0; i < RY; ++i) q[i][uq] = ld2(P + i * TXP);
             const uint32_t slotR = ru.slot >= (uint32_t)R ? ru.slot - R : ru.slot + SU - R;  // plane p-R
             if (k >= 2 * R) {
                 const int z = zb + k - 2 * R;  // output plane
-                const float* Qs = ring + slotR * C::STAGE_STRIDE_F + ly * TXP + RP + lane;
+                const float* Qs = ring + slotR * C::STAGE_STRIDE_F + ly * TXP + RP + CA * lane;
                 // (u^{n-1}, b, a) tiles of the output plane
                 mbar_wait(&fullP[rp.slot], rp.phase);
-                const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + lane;
+                const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + CA * lane;
                 // stage metadata written by the streams producer before its arrive: use_a, injection list
                 const bool use_a = pmeta[3 * rp.slot] != 0;
                 const int inj_first = pmeta[3 * rp.slot + 1], inj_count = pmeta[3 * rp.slot + 2];
                 // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
                 float2 col[RY + 2 * R];
 #pragma unroll
-                for (int r = 0; r < RY + 2 * R; ++r) col[r] = f2(Qs[r * TXP], Qs[r * TXP + 32]);
+                for (int r = 0; r < RY + 2 * R; ++r) col[r] = ld2(Qs + r * TXP);
                 float2 res[RY];
 #pragma unroll
                 for (int i = 0; i < RY; ++i) {
                     const float* row = Qs + (i + R) * TXP;
                     const float2 uc = q[i][(uq + Q - R) % Q];
                     float2 L = mul2(C0, uc);
+                    if constexpr (C::ADJ) {
+                        // v[K + k] = columns (2l + 2k, 2l + 2k + 1), k = -K..K: x neighbours of both points
+                        constexpr int K = (R + 1) / 2;
+                        float2 v[2 * K + 1];
 #pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = fma2(f2(A.c.C[2][j], A.c.C[2][j]),
-                                 add2(f2(row[-j], row[32 - j]), f2(row[j], row[32 + j])), L);
+                        for (int k = -K; k <= K; ++k) v[K + k] = *reinterpret_cast<const float2*>(row + 2 * k);
+#pragma unroll
+                        for (int j = 1; j <= R; ++j) {
+                            const int m = j >> 1;
+                            // pair sums u[x-j] + u[x+j] of column 2l (.x) and 2l+1 (.y)
+                            const float2 lo = (j & 1) ? f2(v[K - m - 1].y, v[K - m].x) : v[K - m];
+                            const float2 hi = (j & 1) ? f2(v[K + m].y, v[K + m + 1].x) : v[K + m];
+                            L = fma2(f2(A.c.C[2][j], A.c.C[2][j]), add2(lo, hi), L);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 1; j <= R; ++j)
+                            L = fma2(f2(A.c.C[2][j], A.c.C[2][j]),
+                                     add2(f2(row[-j], row[32 - j]), f2(row[j], row[32 + j])), L);
+                    }
 #pragma unroll
                     for (int j = 1; j <= R; ++j)
                         L = fma2(f2(A.c.C[1][j], A.c.C[1][j]), add2(col[i + R - j], col[i + R + j]), L);
@@ -283,9 +310,9 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                         L = fma2(f2(A.c.C[0][j], A.c.C[0][j]),
                                  add2(q[i][(uq + Q - R - j) % Q], q[i][(uq + Q - R + j) % Q]), L);
                     const float* pr = Pp + i * TX;
-                    const float2 um = f2(pr[0], pr[32]);
-                    const float2 bb = f2(pr[C::PTILE_FLOATS], pr[C::PTILE_FLOATS + 32]);
-                    const float2 aa = use_a ? f2(pr[2 * C::PTILE_FLOATS], pr[2 * C::PTILE_FLOATS + 32]) : one;
+                    const float2 um = ld2(pr);
+                    const float2 bb = ld2(pr + C::PTILE_FLOATS);
+                    const float2 aa = use_a ? ld2(pr + 2 * C::PTILE_FLOATS) : one;
                     // t = 2u - u^{n-1} (2u exact: one rounding), w = fma(b, L, t)
                     const float2 t = fma2(two, uc, f2(-um.x, -um.y));
                     const float2 wv = fma2(bb, L, t);
@@ -300,13 +327,15 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                 for (int e = inj_first; e < inj_first + inj_count; ++e) {
                     const int4 en = A.tpe[e];
                     const int yl = en.x >> 6, xl = en.x & 63;
+                    const int owner = C::ADJ ? xl >> 1 : xl & 31;
+                    const bool second = C::ADJ ? (xl & 1) : (xl >= 32);
 #pragma unroll
                     for (int i = 0; i < RY; ++i) {
-                        if (yl != ly + i || (xl & 31) != lane) continue;
-                        float v = xl < 32 ? res[i].x : res[i].y;
+                        if (yl != ly + i || owner != lane) continue;
+                        float v = second ? res[i].y : res[i].x;
                         const float* qn = A.wavelet + step_n * A.ns;
                         for (int k = en.y; k < en.z; ++k) v = __fmaf_rn(A.inj_s[k], qn[A.inj_src[k]], v);
-                        if (xl < 32) res[i].x = v; else res[i].y = v;
+                        if (second) res[i].y = v; else res[i].x = v;
                     }
                 }
                 if (st_policy) {
@@ -314,14 +343,18 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                     for (int i = 0; i < RY; ++i) {
                         float* o = outp + i * pitch;
                         if (ok_a[i]) st_hint(o, res[i].x, st_policy);
-                        if (ok_b[i]) st_hint(o + 32, res[i].y, st_policy);
+                        if (ok_b[i]) st_hint(o + CB, res[i].y, st_policy);
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < RY; ++i) {
                         float* o = outp + i * pitch;
-                        if (ok_a[i]) o[0] = res[i].x;
-                        if (ok_b[i]) o[32] = res[i].y;
+                        if (C::ADJ && ok_a[i] && ok_b[i]) {
+                            *reinterpret_cast<float2*>(o) = res[i];  // 8-B aligned: x0 % 64 == 0, pitch % 32 == 0
+                        } else {
+                            if (ok_a[i]) o[0] = res[i].x;
+                            if (ok_b[i]) o[CB] = res[i].y;
+                        }
                     }
                 }
                 if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
@@ -332,7 +365,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
 #pragma unroll
                     for (int i = 0; i < RY; ++i) {
                         if (ok_a[i]) h[i * pitch] = res[i].x;
-                        if (ok_b[i]) h[i * pitch + 32] = res[i].y;
+                        if (ok_b[i]) h[i * pitch + CB] = res[i].y;
                     }
                 }
                 outp += plane;
@@ -952,11 +985,11 @@ using C2 = Cfg<2, 32, 4, 4, 4, 0, 1>;
 using C3 = Cfg<3, 32, 4, 4, 4, 0, 1>;
 using C4 = Cfg<4, 32, 4, 4, 4, 0, 1>;
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
-using C6 = Cfg<6, 32, 4, 2, 3, 0, 1>;
+using C6 = Cfg<6, 32, 4, 2, 3, 0, 1, false>;  // ADJ spills at R=6 (168-register cap)
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
 using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
-using C4v1 = Cfg<4, 32, 4, 3, 4, 0, 1>;
+using C4v1 = Cfg<4, 32, 4, 4, 4, 0, 1, false>;  // round-1 lane mapping (l, l+32)
 using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
 using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
 
