@@ -99,6 +99,7 @@ cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubu
     cudaError_t e = cudaSuccess;
     const StreamOps* ops = stream_ops(p->R);
     if (!ops) return cudaErrorNotSupported;
+    p->map_cache.clear();  // model arrays may have moved
     e = ops->make_maps(p, g, ubuf, b, a);
     if (e != cudaSuccess) return e;
     const int ntiles = p->ntx * p->nty;

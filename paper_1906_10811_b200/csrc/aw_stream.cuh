@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -153,7 +154,9 @@ struct Cfg {
     static constexpr size_t U_BYTES = (size_t)SU * STAGE_STRIDE;
     static constexpr size_t P_BYTES = (size_t)SP * PSTAGE_FLOATS * 4;
     // + full/empty barriers of both rings + 3 metadata words per streams stage
-    static constexpr size_t SMEM = U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + 3 * SP * sizeof(int);
+    // + full/empty barriers of both rings, then (16-B aligned) 4 metadata words per streams stage
+    static constexpr size_t META_OFF = (U_BYTES + P_BYTES + (2 * SU + 2 * SP) * sizeof(uint64_t) + 15) / 16 * 16;
+    static constexpr size_t SMEM = META_OFF + 4 * SP * sizeof(int);
     static_assert(TY % RY == 0, "tile shape");
     static_assert(TXP <= 256 && TYP <= 256, "TMA box dims <= 256");
 };
@@ -270,8 +273,8 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                 mbar_wait(&fullP[rp.slot], rp.phase);
                 const float* Pp = pring + rp.slot * C::PSTAGE_FLOATS + ly * TX + CA * lane;
                 // stage metadata written by the streams producer before its arrive: use_a, injection list
-                const bool use_a = pmeta[3 * rp.slot] != 0;
-                const int inj_first = pmeta[3 * rp.slot + 1], inj_count = pmeta[3 * rp.slot + 2];
+                const bool use_a = pmeta[4 * rp.slot] != 0;
+                const int inj_first = pmeta[4 * rp.slot + 1], inj_count = pmeta[4 * rp.slot + 2];
                 // y column of the output plane (rows ly .. ly+RY-1+2R) at both x columns
                 float2 col[RY + 2 * R];
 #pragma unroll
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     uint64_t* emptyU = fullU + SU;
     uint64_t* fullP = emptyU + SU;
     uint64_t* emptyP = fullP + SP;
-    int* pmeta = reinterpret_cast<int*>(emptyP + SP);
+    int* pmeta = reinterpret_cast<int*>(smem + C::META_OFF);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -478,9 +481,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
                         float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
                         mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
-                        pmeta[3 * rr.slot] = use_a;  // published by the release of the arrive below
-                        pmeta[3 * rr.slot + 1] = tp.x;
-                        pmeta[3 * rr.slot + 2] = tp.y;
+                        // ordered for the consumers by this arrive (release) and their wait (acquire);
+                        // compute-sanitizer racecheck does not model mbarrier phases
+                        pmeta[4 * rr.slot] = use_a;
+                        pmeta[4 * rr.slot + 1] = tp.x;
+                        pmeta[4 * rr.slot + 2] = tp.y;
                         mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
                         tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
                         tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     uint64_t* emptyU = fullU + SU;
     uint64_t* fullP = emptyU + SU;
     uint64_t* emptyP = fullP + SP;
-    int* pmeta = reinterpret_cast<int*>(emptyP + SP);
+    int* pmeta = reinterpret_cast<int*>(smem + C::META_OFF);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -693,9 +698,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
                         float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
                         mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
-                        pmeta[3 * rr.slot] = use_a;
-                        pmeta[3 * rr.slot + 1] = tp.x;
-                        pmeta[3 * rr.slot + 2] = tp.y;
+                        // ordered for the consumers by this arrive (release) and their wait (acquire);
+                        // compute-sanitizer racecheck does not model mbarrier phases
+                        pmeta[4 * rr.slot] = use_a;
+                        pmeta[4 * rr.slot + 1] = tp.x;
+                        pmeta[4 * rr.slot + 2] = tp.y;
                         mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
                         // A: Y is dead after this read, b and a are re-read by B; B: last use of all three
                         const uint64_t pb = isB ? drop : keep;
@@ -766,6 +773,9 @@ struct StreamPlan {
     unsigned long long* tb_done = nullptr;  // [tb_nzc][ntiles] completion epochs of the A items
     unsigned long long tb_epoch = 0;        // last epoch handed out (monotone)
     int tb_Z = 0, tb_nzc = 0, tb_lead = 1;
+    // tensor maps of explicit-buffer launches (FWI history ring, adjoint pair), keyed by
+    // (base pointer, box kind); cleared when the plan is refreshed
+    std::unordered_map<uint64_t, CUtensorMap> map_cache;
 };
 
 namespace {
@@ -892,10 +902,22 @@ cudaError_t launch_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const floa
                         const int64_t* d_base, int step_i, cudaStream_t s) {
     StreamMaps M;
     cudaError_t e;
-    if ((e = encode3d(&M.u, ucur, g, g.nz + 2 * g.R, C::TXP, C::TYP))) return e;
-    if ((e = encode3d(&M.un, uprev, g, g.nz + 2 * g.R, C::TX, C::TY))) return e;
-    if ((e = encode3d(&M.b, b, g, g.nz, C::TX, C::TY))) return e;
-    if ((e = encode3d(&M.a, a ? a : b, g, g.nz, C::TX, C::TY))) return e;
+    // encoding a map costs microseconds of host time per call: cache them per (buffer, box kind)
+    auto cached = [&](CUtensorMap* m, const void* base, int planes, int bx, int by, int kind) -> cudaError_t {
+        const uint64_t key = (uint64_t)(uintptr_t)base ^ (uint64_t)kind;  // bases are 256-B aligned
+        auto it = p->map_cache.find(key);
+        if (it != p->map_cache.end()) {
+            *m = it->second;
+            return cudaSuccess;
+        }
+        cudaError_t r = encode3d(m, base, g, planes, bx, by);
+        if (r == cudaSuccess) p->map_cache.emplace(key, *m);
+        return r;
+    };
+    if ((e = cached(&M.u, ucur, g.nz + 2 * g.R, C::TXP, C::TYP, 1))) return e;
+    if ((e = cached(&M.un, uprev, g.nz + 2 * g.R, C::TX, C::TY, 2))) return e;
+    if ((e = cached(&M.b, b, g.nz, C::TX, C::TY, 3))) return e;
+    if ((e = cached(&M.a, a ? a : b, g.nz, C::TX, C::TY, 4))) return e;
     StreamArgs A;
     std::memset(&A, 0, sizeof A);
     A.g = g;
