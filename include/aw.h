@@ -65,8 +65,9 @@ typedef enum {
 enum { AW_GLOBAL = 0 /* array covers the whole global grid */, AW_LOCAL = 1 /* this rank's slab only */ };
 
 /* stencil kernel selection (aw_set_option AW_OPT_KERNEL) */
-enum { AW_KERNEL_AUTO = 0, AW_KERNEL_V1 = 1 /* one thread per point, reference-grade */,
-       AW_KERNEL_STREAM = 2 /* 2.5D z-streaming TMA kernel (3D) */ };
+enum { AW_KERNEL_AUTO = 0 /* STREAM in 3D, TILE2D in 2D */, AW_KERNEL_V1 = 1 /* one thread per point,
+       reference-grade */, AW_KERNEL_STREAM = 2 /* 2.5D z-streaming TMA kernel (3D) */,
+       AW_KERNEL_TILE2D = 3 /* TMA-tiled 2D kernel (reported by aw_last_run_stats; AUTO selects it) */ };
 
 /* options */
 enum {

@@ -26,7 +26,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 # --- constants (include/aw.h) ---
 AW_OK, AW_EINVAL, AW_ENOMEM, AW_ECUDA, AW_ENCCL, AW_ESTATE, AW_EUNSUPPORTED, AW_ENONFINITE = 0, -1, -2, -3, -4, -5, -6, -7
 AW_GLOBAL, AW_LOCAL = 0, 1
-AW_KERNEL_AUTO, AW_KERNEL_V1, AW_KERNEL_STREAM = 0, 1, 2
+AW_KERNEL_AUTO, AW_KERNEL_V1, AW_KERNEL_STREAM, AW_KERNEL_TILE2D = 0, 1, 2, 3
 AW_OPT_KERNEL, AW_OPT_TIMING, AW_OPT_GRAPH_STEPS, AW_OPT_CHECK_FINITE, AW_OPT_CHECKPOINT_STEPS = 1, 2, 3, 4, 5
 AW_OPT_TEMPORAL, AW_OPT_FWI_ACCUMULATE = 6, 7
 STATUS_NAMES = {0: "AW_OK", -1: "AW_EINVAL", -2: "AW_ENOMEM", -3: "AW_ECUDA", -4: "AW_ENCCL",

@@ -159,6 +159,7 @@ struct aw_grid {
     int opt_check = 1;
     // stream kernel plan
     aw::StreamPlan* plan = nullptr;
+    aw::Tile2DPlan* t2 = nullptr;          // 2D tiled kernel (AUTO in 2D, single slab)
     int eta_tiles_pct = 100;
     int kernel_used = AW_KERNEL_V1;
     // graphs: key = (G << 1) | parity
@@ -526,6 +527,9 @@ aw_status prepare(aw_grid* g, double dt) {
         }
     } else if (g->opt_kernel == AW_KERNEL_STREAM) {
         return fail(AW_EUNSUPPORTED, "the streaming kernel is 3D only");
+    } else if (g->ndim == 2 && g->opt_kernel == AW_KERNEL_AUTO && !team_mode(g)) {
+        if (!g->t2) CK(aw::tile2d_prepare(g->geom, &g->t2));
+        g->kernel_used = AW_KERNEL_TILE2D;
     }
     free_graphs(g);
     g->dt = dt;
@@ -553,6 +557,9 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0
         if (!fused) sp.nrl = sp.nuc = 0;
         CK(aw::launch_stencil_stream(g->plan, g->geom, g->coefs, cur, g->ubuf[cur], g->ubuf[nxt], g->b,
                                      g->have_damp ? g->a : nullptr, g->halo, nxt, sp, g->d_base, i, g->s));
+    } else if (g->kernel_used == AW_KERNEL_TILE2D) {
+        CK(aw::launch_stencil_tile2d(g->t2, g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->ubuf[nxt], g->b,
+                                     g->have_damp ? g->a : nullptr, g->s));
     } else {
         CK(aw::launch_stencil_v1(g->geom, g->coefs, g->ubuf[cur], g->ubuf[nxt], g->ubuf[nxt], g->b,
                                  g->have_damp ? g->a : nullptr,
@@ -828,7 +835,10 @@ aw_status fwi_step(aw_grid* g, const float* ucur, const float* uprev, float* une
         ++*launches;
     } else {
         Halo none{};
-        CK(aw::launch_stencil_v1(g->geom, g->coefs, ucur, uprev, unext, g->b, a, none, 0, g->s));
+        if (g->kernel_used == AW_KERNEL_TILE2D)
+            CK(aw::launch_stencil_tile2d(g->t2, g->geom, g->coefs, ucur, uprev, unext, g->b, a, g->s));
+        else
+            CK(aw::launch_stencil_v1(g->geom, g->coefs, ucur, uprev, unext, g->b, a, none, 0, g->s));
         ++*launches;
         if (sp.nrl + sp.nuc > 0) {
             CK(aw::launch_sparse_step(g->geom, sp, ucur, unext, g->d_base, step_i, none, 0, g->s));
@@ -982,6 +992,7 @@ void aw_grid_destroy(aw_grid* g) {
     if (g->s) cudaStreamSynchronize(g->s);
     free_graphs(g);
     if (g->plan) aw::stream_release(g->plan);
+    aw::tile2d_release(g->t2);
     for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
     free_sources(g);
     free_receivers(g);
@@ -1494,7 +1505,8 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
     CHECK_STATE(g);
     switch (option) {
         case AW_OPT_KERNEL:
-            if (value < AW_KERNEL_AUTO || value > AW_KERNEL_STREAM) return fail(AW_EINVAL, "bad kernel %lld", (long long)value);
+            if (value < AW_KERNEL_AUTO || value > AW_KERNEL_STREAM)  // TILE2D is selected by AUTO (2D)
+                return fail(AW_EINVAL, "bad kernel %lld", (long long)value);
             g->opt_kernel = (int)value;
             g->coeffs_valid = false;
             if (g->plan) {

@@ -113,6 +113,14 @@ cudaError_t launch_stencil_tb(StreamPlan* p, const Geom& g, const Coefs& c, cons
 // re-encode the per-parity maps after the caller permuted its wavefield buffers
 cudaError_t stream_remap(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a);
 
+// 2D tiled kernel (aw_stencil2d.cu): one CTA per 64x32 tile, TMA halo box, packed fp32 on column
+// pairs; explicit buffers (in place when uprev == unext).  Sparse work stays in launch_sparse_step.
+struct Tile2DPlan;
+cudaError_t tile2d_prepare(const Geom& g, Tile2DPlan** plan);
+void tile2d_release(Tile2DPlan* p);
+cudaError_t launch_stencil_tile2d(Tile2DPlan* p, const Geom& g, const Coefs& c, const float* ucur, const float* uprev,
+                                  float* unext, const float* b, const float* a, cudaStream_t s);
+
 // ---- NEXT-3 FWI kernels (aw_fwi.cu) ----
 // G += psi * D,  D = fl32(fl32(u1 - 2 u0) + um1), over the owned planes (wavefield layout inputs,
 // model layout G)
