@@ -18,7 +18,8 @@
 // Kernel: one CTA per 64x32 output tile.  A single TMA 2D box load brings the
 // tile plus its R-wide halo into shared memory (OOB zero fill = the zero
 // padding of PAPER.md:455-491), then 8 warps compute 4 rows x 2 columns each
-// with packed FFMA2/FADD2 on column pairs (x, x+32) and store coalesced rows.
+// with packed FFMA2/FADD2 on adjacent column pairs (2l, 2l+1; 64-bit shared
+// loads and stores) and store coalesced rows.
 // Many CTAs per SM (11-16 KB smem each) overlap their loads; HBM-bound at
 // 8 algorithmic B per point update (read u, write u_next).
 #include <cuda.h>
@@ -47,74 +48,107 @@ struct DiffArgs {
     float* out;               // row-pitched output
     int64_t pitch;
     int nx, ny;               // axis 1 (x, contiguous), axis 0 (rows)
-    int ntx;
+    int ntx, nty;             // 64 x 32 tiles
 };
+
+// TMA ring depth: S = 1 with one CTA per tile (grid = #tiles) is the plain tiled kernel, best for
+// R <= 2 where the kernel is store-bound; S = 3 with a persistent grid overlaps the load of the next
+// tiles with the compute of this one, best for R >= 3 (profiles/r1/diffusion_next2.jsonl)
+template <int R>
+constexpr int diff_stages() { return R <= 2 ? 1 : 3; }
 
 template <int R>
 __global__ void __launch_bounds__(256) diffusion_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ DiffArgs A) {
-    constexpr int TX = 64, TY = 32, RY = 4;
+    constexpr int TX = 64, TY = 32, RY = 4, S = diff_stages<R>();
     constexpr int RP = (R + 3) / 4 * 4;  // TMA inner box row must be a multiple of 32 B
     constexpr int TXP = TX + 2 * RP, TYP = TY + 2 * R;
+    constexpr int STAGE_BYTES = TXP * TYP * 4;
+    constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;
     extern __shared__ __align__(128) unsigned char smem[];
-    float* tile = reinterpret_cast<float*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((TXP * TYP * 4 + 127) / 128) * 128);
-
-    const int x0 = (blockIdx.x % A.ntx) * TX, y0 = (blockIdx.x / A.ntx) * TY;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * STAGE_STRIDE);
+    const int ntiles = A.ntx * A.nty;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32d(bar)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32d(bar)),
-                     "r"(TXP * TYP * 4)
+    // persistent CTA: tiles blockIdx.x, +gridDim.x, ... through a ring of S TMA stages, so the load
+    // of the tiles S ahead overlaps the compute of this one (a one-tile CTA waits for its load)
+    auto issue = [&](int t, int s) {
+        const int x0 = (t % A.ntx) * TX, y0 = (t / A.ntx) * TY;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32d(bar + s)),
+                     "r"(STAGE_BYTES)
                      : "memory");
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];" ::"r"(smem_u32d(tile)),
-            "l"(&tm), "r"(x0 - RP), "r"(y0 - R), "r"(smem_u32d(bar))
+            "[%4];" ::"r"(smem_u32d(smem + s * STAGE_STRIDE)),
+            "l"(&tm), "r"(x0 - RP), "r"(y0 - R), "r"(smem_u32d(bar + s))
             : "memory");
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32d(bar + s)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < S; ++s)
+            if (blockIdx.x + s * gridDim.x < ntiles) issue(blockIdx.x + s * gridDim.x, s);
     }
     __syncthreads();
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it % S;
+    const float* tile = reinterpret_cast<const float*>(smem + s * STAGE_STRIDE);
+    const int x0 = (t % A.ntx) * TX, y0 = (t / A.ntx) * TY;
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
         "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32d(bar))
+        "}\n" ::"r"(smem_u32d(bar + s)), "r"((uint32_t)((it / S) & 1))
         : "memory");
 
+    // lane l owns the adjacent columns x0+2l, x0+2l+1: 64-bit shared loads and global stores
     const int ly = warp * RY;
-    const float* Qs = tile + ly * TXP + RP + lane;  // row ly-R .. of the halo'd tile, column lane
+    constexpr int K = (R + 1) / 2;
+    const float* Qs = tile + ly * TXP + RP + 2 * lane;  // row ly-R .. of the halo'd tile, column pair
     float2 col[RY + 2 * R];
 #pragma unroll
-    for (int r = 0; r < RY + 2 * R; ++r) col[r] = make_float2(Qs[r * TXP], Qs[r * TXP + 32]);
+    for (int r = 0; r < RY + 2 * R; ++r) col[r] = *reinterpret_cast<const float2*>(Qs + r * TXP);
     const float2 C0 = make_float2(A.C0, A.C0), D = make_float2(A.D, A.D);
+    const int xa = x0 + 2 * lane;
 #pragma unroll
     for (int i = 0; i < RY; ++i) {
         const int y = y0 + ly + i;
         const float* row = Qs + (i + R) * TXP;
         const float2 uc = col[i + R];
         float2 L = __fmul2_rn(C0, uc);
+        float2 v[2 * K + 1];  // columns (2l + 2k, 2l + 2k + 1), k = -K..K
 #pragma unroll
-        for (int j = 1; j <= R; ++j)  // axis 1 (x, contiguous) first
-            L = __ffma2_rn(make_float2(A.C[1][j], A.C[1][j]),
-                           __fadd2_rn(make_float2(row[-j], row[32 - j]), make_float2(row[j], row[32 + j])), L);
+        for (int k = -K; k <= K; ++k) v[K + k] = *reinterpret_cast<const float2*>(row + 2 * k);
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {  // axis 1 (x, contiguous) first: u[x-j] + u[x+j] of both columns
+            const int m = j >> 1;
+            const float2 lo = (j & 1) ? make_float2(v[K - m - 1].y, v[K - m].x) : v[K - m];
+            const float2 hi = (j & 1) ? make_float2(v[K + m].y, v[K + m + 1].x) : v[K + m];
+            L = __ffma2_rn(make_float2(A.C[1][j], A.C[1][j]), __fadd2_rn(lo, hi), L);
+        }
 #pragma unroll
         for (int j = 1; j <= R; ++j)  // then axis 0 (rows)
             L = __ffma2_rn(make_float2(A.C[0][j], A.C[0][j]), __fadd2_rn(col[i + R - j], col[i + R + j]), L);
         const float2 un = __ffma2_rn(D, L, uc);
-        if (y < A.ny) {
-            float* o = A.out + (int64_t)y * A.pitch + x0 + lane;
-            if (x0 + lane < A.nx) o[0] = un.x;
-            if (x0 + lane + 32 < A.nx) o[32] = un.y;
+        if (y < A.ny && xa < A.nx) {
+            float* o = A.out + (int64_t)y * A.pitch + xa;
+            if (xa + 1 < A.nx) *reinterpret_cast<float2*>(o) = un;  // 8-B aligned: x0 % 64 == 0, pitch % 32 == 0
+            else o[0] = un.x;
         }
+    }
+    __syncthreads();  // every warp finished reading stage s
+    if (tid == 0 && t + S * (int)gridDim.x < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA rewrite
+        issue(t + S * gridDim.x, s);
+    }
     }
 }
 
 template <int R>
 size_t diff_smem() {
     constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = 32 + 2 * R;
-    return ((TXP * TYP * 4 + 127) / 128) * 128 + 16;
+    return diff_stages<R>() * (((TXP * TYP * 4 + 127) / 128) * 128) + 8 * diff_stages<R>();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -209,8 +243,18 @@ template <int R>
 cudaError_t launch_diff(aw_diffusion* d, int src, cudaStream_t s) {
     aw::DiffArgs A = d->args;
     A.out = d->buf[1 - src];
-    const int nty = (d->ny + 31) / 32;
-    aw::diffusion_kernel<R><<<A.ntx * nty, 256, aw::diff_smem<R>(), s>>>(d->tm[src], A);
+    A.nty = (d->ny + 31) / 32;
+    static int occ = 0, sms = 0;  // resident CTAs per SM of this instance (persistent grid)
+    if (!occ) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aw::diffusion_kernel<R>, 256, aw::diff_smem<R>());
+        if (occ < 1) occ = 1;
+    }
+    const int ntiles = A.ntx * A.nty;
+    const int grid = (aw::diff_stages<R>() == 1 || ntiles < sms * occ) ? ntiles : sms * occ;
+    aw::diffusion_kernel<R><<<grid, 256, aw::diff_smem<R>(), s>>>(d->tm[src], A);
     return cudaGetLastError();
 }
 
