@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaw.so")
 SOURCES = (["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu", "aw_fwi.cu", "aw_stencil2d.cu"]
-           + [f"aw_stream_r{r}.cu" for r in range(1, 9)] + ["aw_stream_r4v.cu"])
+           + [f"aw_stream_r{r}.cu" for r in range(1, 9)] + ["aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"])
 HEADERS = ["aw_internal.h", "aw_stream.cuh", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -40,101 +40,125 @@ struct S2Args {
     const float* b;      // model layout
     const float* a;      // null: no damping
     int64_t pitch;
-    int nx, nz, R, ntx;
+    int nx, nz, R, ntx, ntz;
 };
+
+// TMA ring depth: 1 = one CTA per tile (grid = #tiles); S > 1 = persistent grid whose CTAs prefetch
+// the boxes of their next S-1 tiles.  Measured on 16384^2 (profiles/r1/bench_2d.jsonl): S = 3 is
+// slower here (so 8: 0.85 vs 0.75 ms) -- unlike the diffusion kernel, each tile also issues its own
+// u^{n-1}, b, a loads, which the one-tile CTAs already overlap with the box -- so S = 1 for every R.
+template <int R>
+constexpr int s2_stages() { return 1; }
 
 template <int R>
 __global__ void __launch_bounds__(256) stencil2d_kernel(const __grid_constant__ CUtensorMap tm,
                                                         const __grid_constant__ S2Args A) {
-    constexpr int TX = 64, TY = 32, RY = 4;
+    constexpr int TX = 64, TY = 32, RY = 4, S = s2_stages<R>();
     constexpr int RP = (R + 3) / 4 * 4;  // TMA box rows must be multiples of 32 B
     constexpr int TXP = TX + 2 * RP, TYP = TY + 2 * R;
     constexpr int K = (R + 1) / 2;
+    constexpr int STAGE_BYTES = TXP * TYP * 4;
+    constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;
     extern __shared__ __align__(128) unsigned char smem[];
-    float* tile = reinterpret_cast<float*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((TXP * TYP * 4 + 127) / 128) * 128);
-
-    const int x0 = (blockIdx.x % A.ntx) * TX, z0 = (blockIdx.x / A.ntx) * TY;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S * STAGE_STRIDE);
+    const int ntiles = A.ntx * A.ntz;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2_smem(bar)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s2_smem(bar)),
-                     "r"(TXP * TYP * 4)
+    auto issue = [&](int t, int s) {
+        const int x0 = (t % A.ntx) * TX, z0 = (t / A.ntx) * TY;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s2_smem(bar + s)),
+                     "r"(STAGE_BYTES)
                      : "memory");
         // buffer row of plane z is z + R, so the box of planes [z0-R, z0+TY+R) starts at row z0
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-            "[%4];" ::"r"(s2_smem(tile)),
-            "l"(&tm), "r"(x0 - RP), "r"(z0), "r"(s2_smem(bar))
+            "[%4];" ::"r"(s2_smem(smem + s * STAGE_STRIDE)),
+            "l"(&tm), "r"(x0 - RP), "r"(z0), "r"(s2_smem(bar + s))
             : "memory");
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s2_smem(bar + s)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < S; ++s)
+            if (blockIdx.x + s * (int)gridDim.x < ntiles) issue(blockIdx.x + s * gridDim.x, s);
     }
-    // overlap: this thread's u^{n-1}, b, a pairs while the tile is in flight
+    __syncthreads();  // barriers initialised before anyone waits on them
     const int ly = warp * RY;
-    const int xa = x0 + 2 * lane;
-    const bool inA = xa < A.nx, inB = xa + 1 < A.nx;
-    float2 um[RY], bb[RY], aa[RY];
-#pragma unroll
-    for (int i = 0; i < RY; ++i) {
-        const int z = z0 + ly + i;
-        um[i] = bb[i] = make_float2(0.f, 0.f);
-        aa[i] = make_float2(1.f, 1.f);
-        if (z >= A.nz || !inA) continue;
-        const int64_t o = (int64_t)z * A.pitch + xa;
-        const float* pu = A.uprev + o + (int64_t)R * A.pitch;
-        if (inB) {
-            um[i] = *reinterpret_cast<const float2*>(pu);
-            bb[i] = __ldg(reinterpret_cast<const float2*>(A.b + o));
-            if (A.a) aa[i] = __ldg(reinterpret_cast<const float2*>(A.a + o));
-        } else {
-            um[i].x = pu[0];
-            bb[i].x = __ldg(A.b + o);
-            if (A.a) aa[i].x = __ldg(A.a + o);
-        }
-    }
-    __syncthreads();  // barrier initialised before anyone waits on it
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(s2_smem(bar))
-        : "memory");
-
-    const float* Qs = tile + ly * TXP + RP + 2 * lane;  // plane z0+ly-R, column pair of this lane
-    float2 col[RY + 2 * R];
-#pragma unroll
-    for (int r = 0; r < RY + 2 * R; ++r) col[r] = *reinterpret_cast<const float2*>(Qs + r * TXP);
     const float2 C0 = make_float2(A.c.C0, A.c.C0);
     const float2 two = make_float2(2.f, 2.f), one = make_float2(1.f, 1.f);
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % S;
+        const int x0 = (t % A.ntx) * TX, z0 = (t / A.ntx) * TY;
+        // this thread's u^{n-1}, b, a pairs: issued before waiting for the tile
+        const int xa = x0 + 2 * lane;
+        const bool inA = xa < A.nx, inB = xa + 1 < A.nx;
+        float2 um[RY], bb[RY], aa[RY];
 #pragma unroll
-    for (int i = 0; i < RY; ++i) {
-        const int z = z0 + ly + i;
-        const float* row = Qs + (i + R) * TXP;
-        const float2 uc = col[i + R];
-        float2 L = __fmul2_rn(C0, uc);
-        float2 v[2 * K + 1];
-#pragma unroll
-        for (int k = -K; k <= K; ++k) v[K + k] = *reinterpret_cast<const float2*>(row + 2 * k);
-#pragma unroll
-        for (int j = 1; j <= R; ++j) {  // axis 1 (x) first: pair sums u[x-j] + u[x+j] of both columns
-            const int m = j >> 1;
-            const float2 lo = (j & 1) ? make_float2(v[K - m - 1].y, v[K - m].x) : v[K - m];
-            const float2 hi = (j & 1) ? make_float2(v[K + m].y, v[K + m + 1].x) : v[K + m];
-            L = __ffma2_rn(make_float2(A.c.C[1][j], A.c.C[1][j]), __fadd2_rn(lo, hi), L);
+        for (int i = 0; i < RY; ++i) {
+            const int z = z0 + ly + i;
+            um[i] = bb[i] = make_float2(0.f, 0.f);
+            aa[i] = make_float2(1.f, 1.f);
+            if (z >= A.nz || !inA) continue;
+            const int64_t o = (int64_t)z * A.pitch + xa;
+            const float* pu = A.uprev + o + (int64_t)R * A.pitch;
+            if (inB) {
+                um[i] = *reinterpret_cast<const float2*>(pu);
+                bb[i] = __ldg(reinterpret_cast<const float2*>(A.b + o));
+                if (A.a) aa[i] = __ldg(reinterpret_cast<const float2*>(A.a + o));
+            } else {
+                um[i].x = pu[0];
+                bb[i].x = __ldg(A.b + o);
+                if (A.a) aa[i].x = __ldg(A.a + o);
+            }
         }
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+            "@!P1 bra WAIT_%=;\n"
+            "}\n" ::"r"(s2_smem(bar + s)), "r"((uint32_t)((it / S) & 1))
+            : "memory");
+        const float* tile = reinterpret_cast<const float*>(smem + s * STAGE_STRIDE);
+        const float* Qs = tile + ly * TXP + RP + 2 * lane;  // plane z0+ly-R, column pair of this lane
+        float2 col[RY + 2 * R];
 #pragma unroll
-        for (int j = 1; j <= R; ++j)  // then axis 0 (z)
-            L = __ffma2_rn(make_float2(A.c.C[0][j], A.c.C[0][j]), __fadd2_rn(col[i + R - j], col[i + R + j]), L);
-        const float2 t = __ffma2_rn(two, uc, make_float2(-um[i].x, -um[i].y));  // 2u exact: one rounding
-        const float2 w = __ffma2_rn(bb[i], L, t);
-        const float2 r1 = __fmul2_rn(__fadd2_rn(one, make_float2(-aa[i].x, -aa[i].y)), um[i]);
-        const float2 un = __ffma2_rn(aa[i], w, r1);
-        if (z < A.nz && inA) {
-            float* o = A.unext + (int64_t)(z + R) * A.pitch + xa;
-            if (inB) *reinterpret_cast<float2*>(o) = un;
-            else o[0] = un.x;
+        for (int r = 0; r < RY + 2 * R; ++r) col[r] = *reinterpret_cast<const float2*>(Qs + r * TXP);
+#pragma unroll
+        for (int i = 0; i < RY; ++i) {
+            const int z = z0 + ly + i;
+            const float* row = Qs + (i + R) * TXP;
+            const float2 uc = col[i + R];
+            float2 L = __fmul2_rn(C0, uc);
+            float2 v[2 * K + 1];
+#pragma unroll
+            for (int k = -K; k <= K; ++k) v[K + k] = *reinterpret_cast<const float2*>(row + 2 * k);
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {  // axis 1 (x) first: pair sums u[x-j] + u[x+j] of both columns
+                const int m = j >> 1;
+                const float2 lo = (j & 1) ? make_float2(v[K - m - 1].y, v[K - m].x) : v[K - m];
+                const float2 hi = (j & 1) ? make_float2(v[K + m].y, v[K + m + 1].x) : v[K + m];
+                L = __ffma2_rn(make_float2(A.c.C[1][j], A.c.C[1][j]), __fadd2_rn(lo, hi), L);
+            }
+#pragma unroll
+            for (int j = 1; j <= R; ++j)  // then axis 0 (z)
+                L = __ffma2_rn(make_float2(A.c.C[0][j], A.c.C[0][j]), __fadd2_rn(col[i + R - j], col[i + R + j]), L);
+            const float2 t2 = __ffma2_rn(two, uc, make_float2(-um[i].x, -um[i].y));  // 2u exact: one rounding
+            const float2 w = __ffma2_rn(bb[i], L, t2);
+            const float2 r1 = __fmul2_rn(__fadd2_rn(one, make_float2(-aa[i].x, -aa[i].y)), um[i]);
+            const float2 un = __ffma2_rn(aa[i], w, r1);
+            if (z < A.nz && inA) {
+                float* o = A.unext + (int64_t)(z + R) * A.pitch + xa;
+                if (inB) *reinterpret_cast<float2*>(o) = un;
+                else o[0] = un.x;
+            }
+        }
+        if (S > 1) {
+            __syncthreads();  // every warp finished reading stage s
+            if (tid == 0 && t + S * (int)gridDim.x < ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA rewrite
+                issue(t + S * gridDim.x, s);
+            }
         }
     }
 }
@@ -142,7 +166,7 @@ __global__ void __launch_bounds__(256) stencil2d_kernel(const __grid_constant__ 
 template <int R>
 constexpr size_t s2_smem_bytes() {
     constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = 32 + 2 * R;
-    return ((TXP * TYP * 4 + 127) / 128) * 128 + 16;
+    return s2_stages<R>() * (((TXP * TYP * 4 + 127) / 128) * 128) + 8 * s2_stages<R>();
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 s2_encode_fn() {
@@ -188,7 +212,18 @@ cudaError_t s2_launch(Tile2DPlan* p, const Geom& g, const Coefs& c, const float*
     A.R = g.R;
     A.ntx = p->ntx;
     static_assert(s2_smem_bytes<R>() <= 48 * 1024, "fits the default dynamic shared memory limit");
-    stencil2d_kernel<R><<<p->ntx * p->ntz, 256, s2_smem_bytes<R>(), s>>>(it->second, A);
+    A.ntz = p->ntz;
+    static int occ = 0, sms = 0;  // resident CTAs per SM of this instance (persistent grid for R >= 3)
+    if (!occ) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_kernel<R>, 256, s2_smem_bytes<R>());
+        if (occ < 1) occ = 1;
+    }
+    const int ntiles = p->ntx * p->ntz;
+    const int grid = (s2_stages<R>() == 1 || ntiles < sms * occ) ? ntiles : sms * occ;
+    stencil2d_kernel<R><<<grid, 256, s2_smem_bytes<R>(), s>>>(it->second, A);
     return cudaGetLastError();
 }
 

@@ -1007,13 +1007,20 @@ using C2 = Cfg<2, 32, 4, 4, 4, 0, 1>;
 using C3 = Cfg<3, 32, 4, 4, 4, 0, 1>;
 using C4 = Cfg<4, 32, 4, 4, 4, 0, 1>;
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
-using C6 = Cfg<6, 32, 4, 2, 3, 0, 1, false>;  // ADJ spills at R=6 (168-register cap)
+using C6 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // 0.52 vs 0.56 ms (TY 32, RY 4, spills) on 512^3 (profiles/r1)
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
 using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
 using C4v1 = Cfg<4, 32, 4, 4, 4, 0, 1, false>;  // round-1 lane mapping (l, l+32)
 using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
 using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
+// measurement variants of the high orders (AW_STREAM_VARIANT=1/2/3 with R = 6 / 8)
+using C6v1 = Cfg<6, 32, 4, 2, 3, 0, 1, false>;  // the round-1 R=6 configuration
+using C6v2 = Cfg<6, 16, 2, 3, 3, 0, 1>;
+using C6v3 = Cfg<6, 32, 2, 2, 2, 0, 1>;
+using C8v1 = Cfg<8, 16, 2, 3, 3, 0, 1>;
+using C8v2 = Cfg<8, 32, 2, 1, 2, 0, 1>;
+using C8v3 = Cfg<8, 16, 2, 4, 4, 0, 1, false>;
 
 int variant() {
     const char* v = getenv("AW_STREAM_VARIANT");
