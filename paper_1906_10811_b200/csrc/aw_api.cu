@@ -1291,6 +1291,9 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     }
     const int K = g->stats.fwi_checkpoint;
     const int nseg = (nt + K - 1) / K;
+    // segments: the first one takes the remainder, all later ones K steps, so the last segment -- the
+    // one still in the ring after the forward pass -- is full and only nt - K steps are replayed
+    auto seg_lo = [&](int j) { return j == 0 ? 0 : (j >= nseg ? nt : nt - (nseg - j) * K); };
     const int S = K + 2;
     const int64_t ufl = (int64_t)(g->ubytes / sizeof(float));
     const int64_t own_off = (int64_t)g->R * g->geom.plane;                // first owned plane
@@ -1334,8 +1337,8 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
         if ((st = fwi_step(g, slot(n), slot(n - 1), slot(n + 1), fwd, 0, n, &launches))) return st;
         ++steps_done;
         const int l = n + 1;
-        if (l % K == 0 && l < nt) {  // level jK of segment j = l/K >= 1: keep (u^{jK-1}, u^{jK})
-            const int j = l / K;
+        if (l < nt && (nt - l) % K == 0) {  // l = seg_lo(j), j >= 1: keep (u^{l-1}, u^l)
+            const int j = nseg - (nt - l) / K;
             if ((st = copy_level(ckpt(j, 0), slot(l - 1))) || (st = copy_level(ckpt(j, 1), slot(l)))) return st;
         }
     }
@@ -1349,7 +1352,7 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     CK(cudaMemsetAsync(d_G, 0, g->mbytes, g->s));
     int pc = 0;  // psi^k in psi[pc], psi^{k-1} in psi[1-pc]
     for (int j = nseg - 1; j >= 0; --j) {
-        const int lo = j * K, hi = std::min(lo + K, nt);
+        const int lo = seg_lo(j), hi = seg_lo(j + 1);
         if (j < nseg - 1) {  // recompute levels lo+1 .. hi from the checkpoint
             if (j == 0) {
                 if ((st = zero_level(-1)) || (st = zero_level(0))) return st;
