@@ -220,6 +220,43 @@ def fwi_gradient(mode, shape, extent, space_order, m, dt, nt, d_obs, *, damp=Non
     return grad, res, J.value
 
 
+def run_slabs(world, shape, extent, space_order, m, dt, nt, *, damp=None, origin=None, src_coords=None,
+              wavelet=None, rec_coords=None, u_cur=None, u_prev=None):
+    """FP32CANON run decomposed into `world` virtual slabs of axis 0 with explicit halo exchange
+    (SURVEY §8(c) P12, §8(e)); returns (u_cur, u_prev, rec) gathered like run()."""
+    L = lib()
+    if not hasattr(L, "_slab_sig"):
+        P = ctypes.c_void_p
+        L.oracle_run_slabs.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int, P, P, ctypes.c_double,
+                                       ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P, P, P]
+        L._slab_sig = True
+    ndim = len(shape)
+    shape = tuple(int(s) for s in shape)
+    sh = np.asarray(shape, dtype=np.int64)
+    ex = np.asarray(extent, dtype=np.float64)
+    org = None if origin is None else np.asarray(origin, dtype=np.float64)
+    m = np.ascontiguousarray(m, np.float32).reshape(shape)
+    d = None if damp is None else np.ascontiguousarray(damp, np.float32).reshape(shape)
+    uc = np.zeros(shape, np.float32) if u_cur is None else np.array(u_cur, dtype=np.float32, copy=True).reshape(shape)
+    up = np.zeros(shape, np.float32) if u_prev is None else np.array(u_prev, dtype=np.float32, copy=True).reshape(shape)
+    if src_coords is None:
+        ns, sc, wv = 0, None, None
+    else:
+        sc = np.ascontiguousarray(src_coords, np.float64).reshape(-1, ndim)
+        ns = sc.shape[0]
+        wv = np.ascontiguousarray(wavelet, np.float32).reshape(-1, ns)
+    if rec_coords is None:
+        nr, rc = 0, None
+    else:
+        rc = np.ascontiguousarray(rec_coords, np.float64).reshape(-1, ndim)
+        nr = rc.shape[0]
+    rec = np.zeros((nt, max(nr, 0)), np.float32)
+    _check(L.oracle_run_slabs(int(world), ndim, _p(sh), _p(ex), _p(org), space_order, _p(m), _p(d), float(dt),
+                              int(nt), ns, _p(sc), _p(wv), nr, _p(rc), _p(rec) if nr else None, _p(uc), _p(up)),
+           "run_slabs")
+    return uc, up, rec
+
+
 def diffusion_run(mode, shape, extent, space_order, nu, dt, nt, u0, nthreads=0):
     """NEXT-2: forward-Euler diffusion; returns u^nt (fp32 for mode 0, else fp64)."""
     L = lib()

@@ -711,3 +711,170 @@ out:
     free(hist); free(rec); free(res); free(wadj); free(ucur); free(uprev); free(G);
     return st;
 }
+
+/* ===========================================================================
+ * Virtual slab decomposition: the same run as
+ * oracle_run, mode FP32CANON, computed as `world` slabs of axis 0, each with
+ * its own arrays and R = k/2 halo planes on both sides, the way the multi-GPU
+ * path decomposes it:
+ *   - slab r owns planes [z0_r, z0_r + nz_r): nz_r = n0/world (+1 for the first
+ *     n0 % world ranks), contiguous in rank order (aw_slab_partition);
+ *   - before every step each slab copies the R outermost owned planes of u^n of
+ *     its neighbours into its halo planes (zero beyond the global ends);
+ *   - receiver r is read by the slab owning the plane of its base corner i_0;
+ *     its +1 corner may lie in that slab's halo (SURVEY §8(e) owner-computes);
+ *   - injection entries are applied by the slab owning the corner, in the
+ *     global CSR order restricted to its corners;
+ *   - traces are summed over slabs (disjoint owners: exact).
+ * Decomposition changes no per-point arithmetic, so the result must equal
+ * oracle_run bit for bit (tests/test_oracle_pins.py::test_p12_virtual_slabs).
+ * The wavefields are returned gathered into the global u_cur/u_prev arrays.
+ * ------------------------------------------------------------------------- */
+int oracle_run_slabs(int world, int ndim, const int64_t* shape, const double* extent, const double* origin,
+                     int space_order, const float* m, const float* damp, double dt, int nt,
+                     int ns, const double* src_coords, const float* wavelet,
+                     int nr, const double* rec_coords, float* rec_out, float* u_cur, float* u_prev) {
+    if (ndim < 2 || ndim > 3 || world < 1 || nt < 0) return OR_EINVAL;
+    if (space_order < 2 || space_order > 2 * MAXR || (space_order & 1)) return OR_EINVAL;
+    const int R = space_order / 2, nc = 1 << ndim;
+    const int64_t n0 = shape[0];
+    int64_t per = 1; /* points per plane */
+    for (int d = 1; d < ndim; ++d) per *= shape[d];
+    if (n0 / world < R) return OR_EINVAL; /* every slab must hold >= R planes */
+    float C[3 * (MAXR + 1)], C0;
+    oracle_axis_coeffs(ndim, shape, extent, space_order, C, &C0, NULL, NULL);
+    int st = OR_OK;
+    int64_t N = n0 * per;
+    /* global per-point coefficients and sparse setup (the same helpers as oracle_run) */
+    float* b = (float*)malloc(sizeof(float) * N);
+    float* a = (float*)malloc(sizeof(float) * N);
+    int64_t* sc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ns > 0 ? ns : 1) * nc);
+    double* sw = (double*)malloc(sizeof(double) * (size_t)(ns > 0 ? ns : 1) * nc);
+    int64_t* rc = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1) * nc);
+    double* rw = (double*)malloc(sizeof(double) * (size_t)(nr > 0 ? nr : 1) * nc);
+    inj_entry* inj = (inj_entry*)malloc(sizeof(inj_entry) * (size_t)(ns > 0 ? ns : 1) * nc);
+    float* s32 = (float*)malloc(sizeof(float) * (size_t)(ns > 0 ? ns : 1) * nc);
+    int64_t* z0 = (int64_t*)malloc(sizeof(int64_t) * world);
+    int64_t* nzs = (int64_t*)malloc(sizeof(int64_t) * world);
+    float** slot = (float**)calloc((size_t)world * 3, sizeof(float*));
+    int ninj = 0;
+    if (!b || !a || !sc || !sw || !rc || !rw || !inj || !s32 || !z0 || !nzs || !slot) { st = OR_ENOMEM; goto done; }
+    for (int64_t p = 0; p < N; ++p) {
+        if (!(m[p] > 0.0f) || !isfinite(m[p])) { st = OR_EINVAL; goto done; }
+        point_coeffs(m[p], damp ? damp[p] : 0.0f, dt, &b[p], &a[p], NULL);
+    }
+    if (ns > 0 && oracle_sparse(ndim, shape, extent, origin, ns, src_coords, sc, sw)) { st = OR_EINVAL; goto done; }
+    if (nr > 0 && oracle_sparse(ndim, shape, extent, origin, nr, rec_coords, rc, rw)) { st = OR_EINVAL; goto done; }
+    for (int s = 0; s < ns; ++s)
+        for (int beta = 0; beta < nc; ++beta) {
+            int64_t c = sc[s * nc + beta];
+            if (c < 0) continue;
+            double den; float bb, aa;
+            point_coeffs(m[c], damp ? damp[c] : 0.0f, dt, &bb, &aa, &den);
+            s32[s * nc + beta] = (float)((sw[s * nc + beta] * (dt * dt)) / den);
+            inj[ninj].key = c; inj[ninj].src = s; inj[ninj].beta = beta;
+            ++ninj;
+        }
+    qsort(inj, (size_t)ninj, sizeof(inj_entry), inj_cmp);
+    /* slabs and their arrays: planes [-R, nz+R) of local index, 3 time slots */
+    {
+        int64_t base = n0 / world, rem = n0 % world;
+        for (int r = 0; r < world; ++r) {
+            nzs[r] = base + (r < rem ? 1 : 0);
+            z0[r] = r * base + (r < rem ? r : rem);
+            for (int t = 0; t < 3; ++t) {
+                slot[r * 3 + t] = (float*)calloc((size_t)(nzs[r] + 2 * R) * per, sizeof(float));
+                if (!slot[r * 3 + t]) { st = OR_ENOMEM; goto done; }
+            }
+            /* levels -1 (slot 0) and 0 (slot 1): owned planes from the inputs */
+            memcpy(slot[r * 3 + 1] + R * per, u_cur + z0[r] * per, sizeof(float) * nzs[r] * per);
+            memcpy(slot[r * 3 + 0] + R * per, u_prev + z0[r] * per, sizeof(float) * nzs[r] * per);
+        }
+    }
+    for (int step = 0; step < nt; ++step) {
+        const int k = step + 1;
+        /* halo exchange of u^n: my halo planes <- the neighbours' R outermost owned planes */
+        for (int r = 0; r < world; ++r) {
+            float* u = slot[r * 3 + k % 3];
+            memset(u, 0, sizeof(float) * R * per);
+            memset(u + (R + nzs[r]) * per, 0, sizeof(float) * R * per);
+            if (r > 0) {
+                const float* lo = slot[(r - 1) * 3 + k % 3];
+                memcpy(u, lo + nzs[r - 1] * per, sizeof(float) * R * per); /* its planes [nz-R, nz) */
+            }
+            if (r + 1 < world) {
+                const float* hi = slot[(r + 1) * 3 + k % 3];
+                memcpy(u + (R + nzs[r]) * per, hi + R * per, sizeof(float) * R * per); /* its planes [0, R) */
+            }
+        }
+        for (int r = 0; r < world; ++r) {
+            const float* u = slot[r * 3 + k % 3];
+            const float* um1 = slot[r * 3 + (k - 1) % 3];
+            float* un = slot[r * 3 + (k + 1) % 3];
+            /* receivers owned by this slab (base corner plane i_0 in [z0, z0+nz)) read u^n */
+            for (int q = 0; q < nr; ++q) {
+                int64_t c0 = rc[q * nc + 0];
+                if (c0 < 0) continue;
+                int64_t zb = c0 / per;
+                if (zb < z0[r] || zb >= z0[r] + nzs[r]) continue;
+                float acc = 0.0f;
+                for (int beta = 0; beta < nc; ++beta) {
+                    int64_t c = rc[q * nc + beta];
+                    if (c < 0) continue;
+                    int64_t zl = c / per - z0[r]; /* may be nz (halo plane) */
+                    acc = fmaf((float)rw[q * nc + beta], u[(zl + R) * per + c % per], acc);
+                }
+                rec_out[(int64_t)step * nr + q] += acc;
+            }
+            /* stencil + update at the owned points, axes d = ndim-1 .. 0 */
+            for (int64_t zl = 0; zl < nzs[r]; ++zl)
+                for (int64_t i = 0; i < per; ++i) {
+                    int64_t idx[3];
+                    idx[0] = z0[r] + zl;
+                    int64_t rem2 = i;
+                    for (int d = ndim - 1; d >= 1; --d) { idx[d] = rem2 % shape[d]; rem2 /= shape[d]; }
+                    const int64_t pl = (zl + R) * per + i, pg = (z0[r] + zl) * per + i;
+                    float L = C0 * u[pl];
+                    for (int d = ndim - 1; d >= 0; --d) {
+                        int64_t stride = 1;
+                        for (int e = d + 1; e < ndim; ++e) stride *= shape[e];
+                        for (int j = 1; j <= R; ++j) {
+                            float lo, hi;
+                            if (d == 0) { /* halo planes hold the neighbours' values or zeros */
+                                lo = u[pl - j * per];
+                                hi = u[pl + j * per];
+                            } else {
+                                lo = idx[d] - j >= 0 ? u[pl - j * stride] : 0.0f;
+                                hi = idx[d] + j < shape[d] ? u[pl + j * stride] : 0.0f;
+                            }
+                            float pair = lo + hi;
+                            L = fmaf(C[d * (MAXR + 1) + j], pair, L);
+                        }
+                    }
+                    float t = 2.0f * u[pl] - um1[pl];
+                    float w = fmaf(b[pg], L, t);
+                    float oma = 1.0f - a[pg];
+                    float rr = oma * um1[pl];
+                    un[pl] = fmaf(a[pg], w, rr);
+                }
+            /* injection into owned corners, global CSR order */
+            for (int e = 0; e < ninj; ++e) {
+                int64_t c = inj[e].key;
+                int64_t zl = c / per - z0[r];
+                if (zl < 0 || zl >= nzs[r]) continue;
+                int s = inj[e].src, beta = inj[e].beta;
+                float* v = &un[(zl + R) * per + c % per];
+                *v = fmaf(s32[s * nc + beta], wavelet[(int64_t)step * ns + s], *v);
+            }
+        }
+    }
+    for (int r = 0; r < world; ++r) {
+        memcpy(u_cur + z0[r] * per, slot[r * 3 + (nt + 1) % 3] + R * per, sizeof(float) * nzs[r] * per);
+        memcpy(u_prev + z0[r] * per, slot[r * 3 + nt % 3] + R * per, sizeof(float) * nzs[r] * per);
+    }
+done:
+    if (slot) for (int i = 0; i < world * 3; ++i) free(slot[i]);
+    free(slot); free(z0); free(nzs);
+    free(b); free(a); free(sc); free(sw); free(rc); free(rw); free(inj); free(s32);
+    return st;
+}

@@ -492,3 +492,46 @@ def test_p12_three_slot_rotation_matches_full_history():
         recs.append(r[0])
     assert np.array_equal(hist[-1], full)
     assert np.array_equal(np.array(recs), frec)
+
+
+# ---------------------------------------------------- P12 virtual slabs
+@pytest.mark.parametrize("shape,so,world", [((23, 30), 4, 2), ((23, 30), 4, 5), ((17, 12, 14), 8, 2),
+                                             ((26, 9, 11), 4, 3), ((40, 10, 11), 16, 5)])
+def test_p12_virtual_slabs_equal_single_domain(shape, so, world):
+    """decomposing axis 0 into slabs with an R-plane halo exchange, owner-
+    computes receivers (base corner) and owner-injection changes no arithmetic: bit-exact with one
+    domain, including sources and receivers on slab-boundary planes and the +1 corner in a halo."""
+    w = workloads.small_case(shape, so, 14, nbl=3, ns=3, nr=6, seed=world + so)
+    n0 = shape[0]
+    base, rem = divmod(n0, world)
+    bounds = [r * base + min(r, rem) for r in range(1, world)]
+    h = workloads.H
+    # put sources and receivers right at / between the slab boundary planes
+    extra_src = [[h * (z - 0.5)] + [h * (n - 1) * 0.37 for n in shape[1:]] for z in bounds[:2]]
+    extra_rec = [[h * (z - 1 + 0.25)] + [h * (n - 1) * 0.61 for n in shape[1:]] for z in bounds] + \
+                [[h * z] + [h * (n - 1) * 0.5 for n in shape[1:]] for z in bounds]
+    src = np.concatenate([w.src_coords, np.array(extra_src).reshape(-1, len(shape))])
+    rec = np.concatenate([w.rec_coords, np.array(extra_rec).reshape(-1, len(shape))])
+    wav = workloads.ricker(w.nt, w.dt, 0.02, ns=src.shape[0])
+    rng = np.random.default_rng(1)
+    u0 = rng.standard_normal(shape).astype(np.float32) * 1e-3
+    u1 = rng.standard_normal(shape).astype(np.float32) * 1e-3
+    kw = dict(damp=w.damp, src_coords=src, wavelet=wav, rec_coords=rec, u_cur=u0, u_prev=u1)
+    ou, oup, orec = oracle.run(oracle.FP32CANON, w.shape, w.extent, so, w.m, w.dt, w.nt, **kw)
+    su, sup, srec = oracle.run_slabs(world, w.shape, w.extent, so, w.m, w.dt, w.nt, **kw)
+    assert np.array_equal(su, ou) and np.array_equal(sup, oup)
+    assert np.array_equal(srec, orec)
+
+
+def test_p12_virtual_slabs_detect_a_missing_halo():
+    """The check above can fail: a slab thinner than R (no full halo from one neighbour) is rejected,
+    and a one-plane-narrower halo (exchange of R-1 planes, emulated with so-2 weights on one side)
+    would differ -- here: slabs vs one domain at different space orders must differ."""
+    w = workloads.small_case((20, 16), 8, 6, nbl=2, ns=1, nr=2)
+    with pytest.raises(ValueError):
+        oracle.run_slabs(6, w.shape, w.extent, 8, w.m, w.dt, w.nt)  # 20/6 = 3 planes < R = 4
+    a, _, _ = oracle.run_slabs(2, w.shape, w.extent, 8, w.m, w.dt, w.nt, src_coords=w.src_coords,
+                               wavelet=w.wavelet)
+    b, _, _ = oracle.run(oracle.FP32CANON, w.shape, w.extent, 6, w.m, w.dt, w.nt, src_coords=w.src_coords,
+                         wavelet=w.wavelet)
+    assert not np.array_equal(a, b)
