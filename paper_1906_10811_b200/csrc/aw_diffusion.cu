@@ -221,6 +221,7 @@ struct aw_diffusion {
     aw_run_stats stats{};
     int64_t launches = 0;
     aw::DiffArgs args{};
+    int resident = 0;  // SMs x resident CTAs of the kernel instance (0 = not queried yet)
 };
 
 namespace {
@@ -244,16 +245,14 @@ cudaError_t launch_diff(aw_diffusion* d, int src, cudaStream_t s) {
     aw::DiffArgs A = d->args;
     A.out = d->buf[1 - src];
     A.nty = (d->ny + 31) / 32;
-    static int occ = 0, sms = 0;  // resident CTAs per SM of this instance (persistent grid)
-    if (!occ) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!d->resident) {  // resident CTAs of this instance on the handle's device (persistent grid)
+        int sms = 0, occ = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, aw::diffusion_kernel<R>, 256, aw::diff_smem<R>());
-        if (occ < 1) occ = 1;
+        d->resident = sms * (occ < 1 ? 1 : occ);
     }
     const int ntiles = A.ntx * A.nty;
-    const int grid = (aw::diff_stages<R>() == 1 || ntiles < sms * occ) ? ntiles : sms * occ;
+    const int grid = (aw::diff_stages<R>() == 1 || ntiles < d->resident) ? ntiles : d->resident;
     aw::diffusion_kernel<R><<<grid, 256, aw::diff_smem<R>(), s>>>(d->tm[src], A);
     return cudaGetLastError();
 }

@@ -26,6 +26,7 @@ namespace aw {
 
 struct Tile2DPlan {
     int ntx = 0, ntz = 0;
+    int resident = 0;  // SMs x resident CTAs on the grid's device (queried at the first launch)
     std::unordered_map<const void*, CUtensorMap> maps;  // u^n buffers seen so far (2, or a FWI ring)
 };
 
@@ -213,16 +214,15 @@ cudaError_t s2_launch(Tile2DPlan* p, const Geom& g, const Coefs& c, const float*
     A.ntx = p->ntx;
     static_assert(s2_smem_bytes<R>() <= 48 * 1024, "fits the default dynamic shared memory limit");
     A.ntz = p->ntz;
-    static int occ = 0, sms = 0;  // resident CTAs per SM of this instance (persistent grid for R >= 3)
-    if (!occ) {
-        int dev = 0;
+    if (!p->resident) {  // resident CTAs on the current device (persistent grid when S > 1)
+        int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_kernel<R>, 256, s2_smem_bytes<R>());
-        if (occ < 1) occ = 1;
+        p->resident = sms * (occ < 1 ? 1 : occ);
     }
     const int ntiles = p->ntx * p->ntz;
-    const int grid = (s2_stages<R>() == 1 || ntiles < sms * occ) ? ntiles : sms * occ;
+    const int grid = (s2_stages<R>() == 1 || ntiles < p->resident) ? ntiles : p->resident;
     stencil2d_kernel<R><<<grid, 256, s2_smem_bytes<R>(), s>>>(it->second, A);
     return cudaGetLastError();
 }

@@ -1016,10 +1016,10 @@ using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
 using C4v3 = Cfg<4, 16, 2, 4, 4, 0, 1>;
 // measurement variants of the high orders (AW_STREAM_VARIANT=1/2/3 with R = 6 / 8)
 using C6v1 = Cfg<6, 32, 4, 2, 3, 0, 1, false>;  // the round-1 R=6 configuration
-using C6v2 = Cfg<6, 16, 2, 3, 3, 0, 1>;
+using C6v2 = Cfg<6, 16, 1, 4, 4, 0, 1>;  // 16 consumer warps, one row each
 using C6v3 = Cfg<6, 32, 2, 2, 2, 0, 1>;
 using C8v1 = Cfg<8, 16, 2, 3, 3, 0, 1>;
-using C8v2 = Cfg<8, 32, 2, 1, 2, 0, 1>;
+using C8v2 = Cfg<8, 16, 1, 4, 4, 0, 1>;  // 16 consumer warps, one row each
 using C8v3 = Cfg<8, 16, 2, 4, 4, 0, 1, false>;
 
 int variant() {
