@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="aw", choices=["aw", "reference"])
-    ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--nt", type=int, default=None, help="override time steps per bench step")
     ap.add_argument("--kernel", default="auto", choices=["auto", "v1", "stream"])
     ap.add_argument("--temporal", type=int, default=0, choices=[0, 1],
@@ -143,6 +143,10 @@ def workload_spec(name, world):
             rec = np.concatenate([rec, np.array([[10.0 * r, 2555.3, 2554.7] for r in range(shape[0])])])
         return dict(name="C3" if N == 1 else f"C3-weak(N={N})", shape=shape, so=8, nt=base.nt, dt=base.dt,
                     f0=base.f0, nbl=32, model="random_smooth", src=src, rec=rec)
+    if name == "C4":  # strong scaling: one 1024^3 grid, split into `world` slabs
+        base = W.c4(with_arrays=False)
+        return dict(name=f"C4(N={world})", shape=base.shape, so=12, nt=base.nt, dt=base.dt, f0=base.f0, nbl=32,
+                    model="random_smooth", src=base.src_coords, rec=base.rec_coords, scaling="strong")
     if name == "C5":
         base = W.c5(N=world, with_arrays=False)
         return dict(name=f"C5(N={world})", shape=base.shape, so=16, nt=base.nt, dt=base.dt, f0=base.f0, nbl=32,
@@ -212,7 +216,7 @@ def run_reference(args, rank, world):
               f"bench step (whole oracle_run call incl. its coefficient setup)")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gpts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "higher_is_better": True, "scaling": spec.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": spec["name"], "shape": list(spec["shape"]), "space_order": spec["so"],
                        "time_steps": nsteps},
             "cpu_baseline": {"value": round(value, 4), "unit": "Gpts/s", "cores": os.cpu_count(), "kind": "oracle",
@@ -406,7 +410,7 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "scaling": spec.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": spec["name"], "shape": list(shape), "space_order": spec["so"],
                            "time_steps": nt, "dt_ms": spec["dt"], "model": spec["model"], "nbl": spec["nbl"],
                            "sources": len(spec["src"]), "receivers": nr, "parallelism": f"slab{world}",

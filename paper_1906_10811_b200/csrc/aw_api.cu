@@ -1238,9 +1238,11 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     if (nt > g->rec_nt) return fail(AW_EINVAL, "trace buffer covers %d steps, need %d", g->rec_nt, nt);
     aw_status st = enter(g);
     if (st) return st;
-    // start from the reset state (zero wavefields, step 0) with this dt
+    // start from the reset state (zero wavefields, step 0) with this dt; until aw_reset /
+    // aw_set_wavefield the wavefield levels are not a forward state (also if this call fails)
     g->steps = 0;
     g->cur = 0;
+    g->wave_invalid = true;
     if (!(g->dt_set && g->dt == dt)) g->coeffs_valid = false;  // any dt: the call starts from the reset state
     if ((st = prepare(g, dt))) return st;
     if ((st = fwi_build_adjoint(g))) return st;
