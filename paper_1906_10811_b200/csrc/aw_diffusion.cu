@@ -35,6 +35,13 @@
 
 extern "C" aw_status aw_internal_fail(aw_status st, const char* msg);
 
+#ifndef AW_DIFF_TALL
+#define AW_DIFF_TALL 1
+#endif
+#ifndef AW_DIFF_TALL_R
+#define AW_DIFF_TALL_R 5  // tall tiles measured slower for R = 3, 4 (profiles/r1/diffusion_next2.jsonl)
+#endif
+
 namespace aw {
 namespace {
 
@@ -56,10 +63,14 @@ struct DiffArgs {
 // tiles with the compute of this one, best for R >= 3 (profiles/r1/diffusion_next2.jsonl)
 template <int R>
 constexpr int diff_stages() { return R <= 2 ? 1 : 3; }
+// tile height: taller tiles halve the y-halo overhead ((TY+2R)/TY) and the per-row column loads
+// ((RY+2R)/RY) at high orders; 8 warps, RY = TY/8 rows per thread
+template <int R>
+constexpr int diff_ty() { return AW_DIFF_TALL && R >= AW_DIFF_TALL_R ? 64 : 32; }
 
 template <int R>
 __global__ void __launch_bounds__(256) diffusion_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ DiffArgs A) {
-    constexpr int TX = 64, TY = 32, RY = 4, S = diff_stages<R>();
+    constexpr int TX = 64, TY = diff_ty<R>(), RY = TY / 8, S = diff_stages<R>();
     constexpr int RP = (R + 3) / 4 * 4;  // TMA inner box row must be a multiple of 32 B
     constexpr int TXP = TX + 2 * RP, TYP = TY + 2 * R;
     constexpr int STAGE_BYTES = TXP * TYP * 4;
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(256) diffusion_kernel(const __grid_constant__ 
 
 template <int R>
 size_t diff_smem() {
-    constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = 32 + 2 * R;
+    constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = diff_ty<R>() + 2 * R;
     return diff_stages<R>() * (((TXP * TYP * 4 + 127) / 128) * 128) + 8 * diff_stages<R>();
 }
 
@@ -244,7 +255,7 @@ template <int R>
 cudaError_t launch_diff(aw_diffusion* d, int src, cudaStream_t s) {
     aw::DiffArgs A = d->args;
     A.out = d->buf[1 - src];
-    A.nty = (d->ny + 31) / 32;
+    A.nty = (d->ny + aw::diff_ty<R>() - 1) / aw::diff_ty<R>();
     if (!d->resident) {  // resident CTAs of this instance on the handle's device (persistent grid)
         int sms = 0, occ = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
@@ -358,7 +369,8 @@ aw_status aw_diffusion_create(aw_diffusion** out, int ndim, const int64_t* shape
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
         cuuint64_t dims[2] = {(cuuint64_t)d->nx, (cuuint64_t)d->ny};
         cuuint64_t strides[1] = {(cuuint64_t)d->pitch * 4};
-        cuuint32_t box[2] = {(cuuint32_t)(64 + 2 * RP), (cuuint32_t)(32 + 2 * R)};
+        const int TY = R >= AW_DIFF_TALL_R && AW_DIFF_TALL ? 64 : 32;  // = aw::diff_ty<R>()
+        cuuint32_t box[2] = {(cuuint32_t)(64 + 2 * RP), (cuuint32_t)(TY + 2 * R)};
         cuuint32_t estr[2] = {1, 1};
         if (!enc || enc(&d->tm[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d->buf[b], dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,

@@ -50,11 +50,17 @@ struct S2Args {
 // u^{n-1}, b, a loads, which the one-tile CTAs already overlap with the box -- so S = 1 for every R.
 template <int R>
 constexpr int s2_stages() { return 1; }
+// tile height (8 warps, TY/8 rows per thread): 64 halves the z-halo overhead at high orders
+#ifndef AW_S2_TALL_R
+#define AW_S2_TALL_R 9  // off: 64-row tiles measured no faster here (so 12: 0.854 vs 0.86 ms on 16384^2)
+#endif
+template <int R>
+constexpr int s2_ty() { return R >= AW_S2_TALL_R ? 64 : 32; }
 
 template <int R>
 __global__ void __launch_bounds__(256) stencil2d_kernel(const __grid_constant__ CUtensorMap tm,
                                                         const __grid_constant__ S2Args A) {
-    constexpr int TX = 64, TY = 32, RY = 4, S = s2_stages<R>();
+    constexpr int TX = 64, TY = s2_ty<R>(), RY = TY / 8, S = s2_stages<R>();
     constexpr int RP = (R + 3) / 4 * 4;  // TMA box rows must be multiples of 32 B
     constexpr int TXP = TX + 2 * RP, TYP = TY + 2 * R;
     constexpr int K = (R + 1) / 2;
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(256) stencil2d_kernel(const __grid_constant__ 
 
 template <int R>
 constexpr size_t s2_smem_bytes() {
-    constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = 32 + 2 * R;
+    constexpr int RP = (R + 3) / 4 * 4, TXP = 64 + 2 * RP, TYP = s2_ty<R>() + 2 * R;
     return s2_stages<R>() * (((TXP * TYP * 4 + 127) / 128) * 128) + 8 * s2_stages<R>();
 }
 
@@ -193,7 +199,7 @@ cudaError_t s2_launch(Tile2DPlan* p, const Geom& g, const Coefs& c, const float*
         CUtensorMap m;
         cuuint64_t dims[2] = {(cuuint64_t)g.nx, (cuuint64_t)(g.nz + 2 * g.R)};
         cuuint64_t strides[1] = {(cuuint64_t)g.pitch * 4};
-        cuuint32_t box[2] = {(cuuint32_t)(64 + 2 * RP), (cuuint32_t)(32 + 2 * R)};
+        cuuint32_t box[2] = {(cuuint32_t)(64 + 2 * RP), (cuuint32_t)(s2_ty<R>() + 2 * R)};
         cuuint32_t estr[2] = {1, 1};
         if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ucur), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -213,7 +219,7 @@ cudaError_t s2_launch(Tile2DPlan* p, const Geom& g, const Coefs& c, const float*
     A.R = g.R;
     A.ntx = p->ntx;
     static_assert(s2_smem_bytes<R>() <= 48 * 1024, "fits the default dynamic shared memory limit");
-    A.ntz = p->ntz;
+    A.ntz = (g.nz + s2_ty<R>() - 1) / s2_ty<R>();
     if (!p->resident) {  // resident CTAs on the current device (persistent grid when S > 1)
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
@@ -221,7 +227,7 @@ cudaError_t s2_launch(Tile2DPlan* p, const Geom& g, const Coefs& c, const float*
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_kernel<R>, 256, s2_smem_bytes<R>());
         p->resident = sms * (occ < 1 ? 1 : occ);
     }
-    const int ntiles = p->ntx * p->ntz;
+    const int ntiles = p->ntx * A.ntz;
     const int grid = (s2_stages<R>() == 1 || ntiles < p->resident) ? ntiles : p->resident;
     stencil2d_kernel<R><<<grid, 256, s2_smem_bytes<R>(), s>>>(it->second, A);
     return cudaGetLastError();
