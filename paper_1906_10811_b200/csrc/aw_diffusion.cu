@@ -134,9 +134,15 @@ __global__ void __launch_bounds__(256) diffusion_kernel(const __grid_constant__ 
 #pragma unroll
         for (int j = 1; j <= R; ++j) {  // axis 1 (x, contiguous) first: u[x-j] + u[x+j] of both columns
             const int m = j >> 1;
-            const float2 lo = (j & 1) ? make_float2(v[K - m - 1].y, v[K - m].x) : v[K - m];
-            const float2 hi = (j & 1) ? make_float2(v[K + m].y, v[K + m + 1].x) : v[K + m];
-            L = __ffma2_rn(make_float2(A.C[1][j], A.C[1][j]), __fadd2_rn(lo, hi), L);
+            if (j & 1) {  // odd j: the two columns' pairs sit in different float2s -- two packed adds,
+                // each keeps one useful half, then scalar fmas (no register moves to re-pair halves)
+                const float2 sa = __fadd2_rn(v[K - m - 1], v[K + m]);      // .y = u[2l-j] + u[2l+j]
+                const float2 sb = __fadd2_rn(v[K - m], v[K + m + 1]);      // .x = u[2l+1-j] + u[2l+1+j]
+                L.x = __fmaf_rn(A.C[1][j], sa.y, L.x);
+                L.y = __fmaf_rn(A.C[1][j], sb.x, L.y);
+            } else {
+                L = __ffma2_rn(make_float2(A.C[1][j], A.C[1][j]), __fadd2_rn(v[K - m], v[K + m]), L);
+            }
         }
 #pragma unroll
         for (int j = 1; j <= R; ++j)  // then axis 0 (rows)

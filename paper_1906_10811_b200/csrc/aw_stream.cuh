@@ -301,9 +301,15 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                         for (int j = 1; j <= R; ++j) {
                             const int m = j >> 1;
                             // pair sums u[x-j] + u[x+j] of column 2l (.x) and 2l+1 (.y)
-                            const float2 lo = (j & 1) ? f2(v[K - m - 1].y, v[K - m].x) : v[K - m];
-                            const float2 hi = (j & 1) ? f2(v[K + m].y, v[K + m + 1].x) : v[K + m];
-                            L = fma2(f2(A.c.C[2][j], A.c.C[2][j]), add2(lo, hi), L);
+                            if (j & 1) {  // odd j: the two columns' pairs sit in different float2s -- two packed adds,
+                                // each keeps one useful half, then scalar fmas (no register moves to re-pair halves)
+                                const float2 sa = add2(v[K - m - 1], v[K + m]);      // .y = u[2l-j] + u[2l+j]
+                                const float2 sb = add2(v[K - m], v[K + m + 1]);      // .x = u[2l+1-j] + u[2l+1+j]
+                                L.x = __fmaf_rn(A.c.C[2][j], sa.y, L.x);
+                                L.y = __fmaf_rn(A.c.C[2][j], sb.x, L.y);
+                            } else {
+                                L = fma2(make_float2(A.c.C[2][j], A.c.C[2][j]), add2(v[K - m], v[K + m]), L);
+                            }
                         }
                     } else {
 #pragma unroll
