@@ -417,6 +417,9 @@ def main():
                            "l2": "inputs larger than L2 (working set %.1f GiB)" % (
                                pts_local * 4 * (4 + (1 if d_dev is not None else 0) * 2) / 2 ** 30)},
                 "hbm_pct_strict": round(100 * value * B_STRICT / world / peak, 2),
+                # SURVEY §8(d) B_alg = 16 + 4 f_eta: the `a` stream is read in the tile-planes that hold damping
+                "hbm_pct_alg": round(100 * value * (B_STRICT + 4 * st["eta_tiles"] / 100.0) / world / peak, 2),
+                "eta_tile_planes_pct": st["eta_tiles"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk}
         print(json.dumps(line), flush=True)
