@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaw.so")
+# AW_LIBRARY: development knob for same-box A/B runs of two builds (tools/ab_stream.py); the default
+# and everything the tests, bench and smoke() load is the in-tree libaw.so
+LIB_PATH = os.environ.get("AW_LIBRARY") or os.path.join(_HERE, "libaw.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
