@@ -197,6 +197,22 @@ def oracle_sample(spec, nsteps):
     return pts / t / 1e9, t, threads
 
 
+def bench_config(spec, nt, world, pts_local, damped):
+    """The `config` object of both arms' JSON lines (workload C1-C5)."""
+    return {"workload": spec["name"], "shape": list(spec["shape"]), "space_order": spec["so"],
+            "time_steps": nt, "dt_ms": spec["dt"], "model": spec["model"], "nbl": spec["nbl"],
+            "sources": len(spec["src"]), "receivers": len(spec["rec"]), "parallelism": f"slab{world}",
+            "l2": l2_note(pts_local * 4 * (4 + (2 if damped else 0)))}
+
+
+def l2_note(ws_bytes):
+    """How the timed steps relate to the 126 MB L2 (bench timing rules)."""
+    if ws_bytes > 126e6:
+        return "inputs larger than L2 (working set %.1f GiB)" % (ws_bytes / 2 ** 30)
+    return ("working set %.1f MiB fits in L2; L2 not flushed between time steps (every step re-reads it, "
+            "as the method does)" % (ws_bytes / 2 ** 20))
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle (CPU) on the same workload, metric and unit."""
     if rank != 0:
@@ -217,8 +233,11 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Gpts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 1),
             "higher_is_better": True, "scaling": spec.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": spec["name"], "shape": list(spec["shape"]), "space_order": spec["so"],
-                       "time_steps": nsteps},
+            # the same workload config as the library arm (the driver pairs the two lines); the bounded
+            # oracle sample per bench step is stated in cpu_baseline.sample
+            "config": bench_config(spec, args.nt or spec["nt"], world,
+                                   float(spec["shape"][0] // world) * float(np.prod(spec["shape"][1:])),
+                                   spec["nbl"] > 0),
             "cpu_baseline": {"value": round(value, 4), "unit": "Gpts/s", "cores": os.cpu_count(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -411,11 +430,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
                 "scaling": spec.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": spec["name"], "shape": list(shape), "space_order": spec["so"],
-                           "time_steps": nt, "dt_ms": spec["dt"], "model": spec["model"], "nbl": spec["nbl"],
-                           "sources": len(spec["src"]), "receivers": nr, "parallelism": f"slab{world}",
-                           "l2": "inputs larger than L2 (working set %.1f GiB)" % (
-                               pts_local * 4 * (4 + (1 if d_dev is not None else 0) * 2) / 2 ** 30)},
+                "config": bench_config(spec, nt, world, pts_local, d_dev is not None),
                 "hbm_pct_strict": round(100 * value * B_STRICT / world / peak, 2),
                 # SURVEY §8(d) B_alg = 16 + 4 f_eta: the `a` stream is read in the tile-planes that hold damping
                 "hbm_pct_alg": round(100 * value * (B_STRICT + 4 * st["eta_tiles"] / 100.0) / world / peak, 2),
