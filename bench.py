@@ -324,8 +324,9 @@ def main():
             if verbose and (dt_ms > 20 and name != "run"):
                 print(f"  slow call {name}: {dt_ms:.1f} ms", file=sys.stderr, flush=True)
 
-    # per-launch CUDA events around the stencil kernel (the event pool is created in the warm-up)
-    g.set_option(aw.AW_OPT_TIMING, 1)
+    # the timed region runs the production path (per-launch timing off: CUDA graphs of several steps
+    # where the library uses them); the roofline pass below repeats the K steps with per-launch events
+    g.set_option(aw.AW_OPT_TIMING, 0)
     for _ in range(args.warmup):
         one_step(m_dev, d_dev, wav_dev, traces_dev)
 
@@ -340,17 +341,12 @@ def main():
         clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    ms_stencil, n_stencil, ms_runs = 0.0, 0, 0.0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         one_step(m_dev, d_dev, wav_dev, traces_dev)
-        st = g.stats()
-        ms_stencil += st["ms_stencil"]
-        n_stencil += st["n_stencil"]
-        ms_runs += st["ms_total"]
-        if os.environ.get("AW_BENCH_VERBOSE"):
-            print(f"step: wall {1e3 * (time.perf_counter() - t0):.2f} ms, run {st['ms_total']:.2f} ms, "
-                  f"stencil {st['ms_stencil']:.2f} ms", file=sys.stderr, flush=True)
+        if verbose:
+            print(f"step: wall {1e3 * (time.perf_counter() - t0):.2f} ms, run {g.stats()['ms_total']:.2f} ms",
+                  file=sys.stderr, flush=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -358,11 +354,28 @@ def main():
     gc.enable()
     ms = ev0.elapsed_time(ev1)
     launches = g.stats()["launches_total"] - launches0
-    st = g.stats()
     if world > 1:
         ms = allreduce_max(ms)
     total_pts = float(np.prod(shape)) * nt * args.steps
     value = total_pts / (ms * 1e-3) / 1e9
+
+    # ---- roofline pass: the same K steps again with per-launch CUDA events on the library's stream ----
+    g.set_option(aw.AW_OPT_TIMING, 1)
+    one_step(m_dev, d_dev, wav_dev, traces_dev)  # creates the event pool
+    torch.cuda.synchronize()
+    barrier()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    ms_stencil, n_stencil = 0.0, 0
+    for _ in range(args.steps):
+        one_step(m_dev, d_dev, wav_dev, traces_dev)
+        st = g.stats()
+        ms_stencil += st["ms_stencil"]
+        n_stencil += st["n_stencil"]
+    r1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_rpass = r0.elapsed_time(r1)
 
     # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region ----
     e2e = None
@@ -413,7 +426,10 @@ def main():
                 "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
                 "kernel": f"stencil_{kname}", "bytes_per_point": bytes_per_launch_pt,
                 "steps_per_launch": steps_per_launch, "peak_source": peak_src,
-                "stencil_ms_avg": round(avg_ms, 4), "stencil_share_of_step": round(ms_stencil / ms, 4) if ms else None,
+                "stencil_ms_avg": round(avg_ms, 4),
+                "stencil_share_of_step": round(ms_stencil / ms_rpass, 4) if ms_rpass else None,
+                "measured_in": "a second pass of the same K bench steps with per-launch CUDA events on the "
+                               "library stream (the headline timed region runs without them)",
                 # the strict one-step streaming floor (16 B per point update) at the achieved update rate
                 "vs_streaming_floor": round(B_STRICT * pts_local / (ms_stencil / max(1, n_stencil) * 1e-3) / 1e9
                                             / peak, 4) if ms_stencil > 0 else None}

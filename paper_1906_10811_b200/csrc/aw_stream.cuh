@@ -222,7 +222,7 @@ struct Ring {
 
 // One work item (xy tile, z chunk) for a consumer thread.  INTERIOR tiles need
 // no bounds predicates.  The ring positions advance exactly like the producer's.
-template <class C, bool INTERIOR, bool TEAM>
+template <class C, bool INTERIOR, bool TEAM, bool HINT = false>
 __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* ring, const float* pring,
                                              uint64_t* fullU, uint64_t* emptyU, uint64_t* fullP, uint64_t* emptyP,
                                              const volatile int* pmeta,
@@ -334,8 +334,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                     const float2 rr = mul2(add2(one, f2(-aa.x, -aa.y)), um);
                     res[i] = fma2(aa, wv, rr);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyP[rp.slot]);
+                mbar_arrive(&emptyP[rp.slot]);  // every consumer thread arrives: no warp sync, no branch
                 rp.advance(SP);
                 // fused injection: u^{n+1}[c] = fma(s, q[n][src], u^{n+1}[c]) over the
                 // corner's sources in CSR order, applied by the thread that owns the corner, before storing
@@ -353,7 +352,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                         if (second) res[i].y = v; else res[i].x = v;
                     }
                 }
-                if (st_policy) {
+                if constexpr (HINT) {
 #pragma unroll
                     for (int i = 0; i < RY; ++i) {
                         float* o = outp + i * pitch;
@@ -387,8 +386,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
             }
             // release the stage of plane p - R (no longer needed by any later output)
             if (k >= R) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyU[slotR]);
+                mbar_arrive(&emptyU[slotR]);
             }
             ru.advance(SU);
         }
@@ -397,8 +395,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
 #pragma unroll 1
     for (int m = 0; m < R; ++m) {
         const uint32_t s = ru.slot >= (uint32_t)(R - m) ? ru.slot - (R - m) : ru.slot + SU - (R - m);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyU[s]);
+        mbar_arrive(&emptyU[s]);
     }
 }
 
@@ -421,11 +418,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     if (tid == 0) {
         for (int s = 0; s < SU; ++s) {
             mbar_init(&fullU[s], 1);
-            mbar_init(&emptyU[s], C::NWARPS_COMP);
+            mbar_init(&emptyU[s], C::NCOMP);  // one arrival per consumer thread
         }
         for (int s = 0; s < SP; ++s) {
             mbar_init(&fullP[s], 1);
-            mbar_init(&emptyP[s], C::NWARPS_COMP);
+            mbar_init(&emptyP[s], C::NCOMP);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -623,11 +620,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     if (tid == 0) {
         for (int s = 0; s < SU; ++s) {
             mbar_init(&fullU[s], 1);
-            mbar_init(&emptyU[s], C::NWARPS_COMP);
+            mbar_init(&emptyU[s], C::NCOMP);  // one arrival per consumer thread
         }
         for (int s = 0; s < SP; ++s) {
             mbar_init(&fullP[s], 1);
-            mbar_init(&emptyP[s], C::NWARPS_COMP);
+            mbar_init(&emptyP[s], C::NCOMP);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -743,10 +740,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             const int64_t n_inj = step_n + (isB ? 1 : 0);
             const uint64_t pol = isB ? st_drop : st_keep;  // V is re-read by B; W only by the next pass
             if (x0 + TX <= g.nx && y0 + TY <= g.ny)
-                consume_item<C, true, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
+                consume_item<C, true, false, true>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
                                              lane, ly, ru, rp, n_inj, out, pol);
             else
-                consume_item<C, false, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
+                consume_item<C, false, false, true>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
                                               y0, lane, ly, ru, rp, n_inj, out, pol);
         }
         if (!isB && c < T.nzc) {
