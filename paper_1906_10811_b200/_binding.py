@@ -129,6 +129,20 @@ def _ptr(a, dtype=np.float32, keep=None):
     return arr.ctypes.data
 
 
+def _out_ptr(a):
+    """Pointer to a caller-provided OUTPUT buffer: it must already be C-contiguous float32 (the C side
+    writes into it), so no temporary copy is ever made."""
+    if hasattr(a, "data_ptr"):  # torch.Tensor
+        import torch
+        if a.dtype != torch.float32 or not a.is_contiguous():
+            raise TypeError("output tensor must be a contiguous torch.float32 tensor")
+        return a.data_ptr()
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"] \
+            or not a.flags["WRITEABLE"]:
+        raise TypeError("output array must be a writeable C-contiguous numpy.float32 array")
+    return a.ctypes.data
+
+
 def _torch_stream_handle(stream):
     """cudaStream_t for a torch stream; the legacy default stream maps to cudaStreamLegacy (0x1)."""
     h = stream.cuda_stream
@@ -223,14 +237,14 @@ class Grid:
         if out is None:
             shp = self.shape if layout == AW_GLOBAL else self.local_shape
             out = np.zeros(shp, np.float32)
-        check(aw_read_wavefield(self.handle, which, _ptr(out), layout))
+        check(aw_read_wavefield(self.handle, which, _out_ptr(out), layout))
         return out
 
     def read_receivers(self, out=None):
         if out is None:
             out = np.zeros((self.steps_done, self.nr), np.float32)
         if self.nr and self.steps_done:
-            check(aw_read_receivers(self.handle, _ptr(out)))
+            check(aw_read_receivers(self.handle, _out_ptr(out)))
         return out
 
     def debug_sparse(self, which):
@@ -257,8 +271,8 @@ class Grid:
         if residual is None and want_residual:
             residual = np.zeros((int(nt), self.nr), np.float32)
         J = _D(0.0)
-        check(aw_fwi_gradient(self.handle, int(nt), float(dt), _ptr(d_obs, keep=keep), _ptr(grad), layout,
-                              _ptr(residual), ctypes.byref(J)))
+        check(aw_fwi_gradient(self.handle, int(nt), float(dt), _ptr(d_obs, keep=keep), _out_ptr(grad), layout,
+                              None if residual is None else _out_ptr(residual), ctypes.byref(J)))
         return grad, residual, J.value
 
     # team plumbing

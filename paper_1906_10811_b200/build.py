@@ -11,17 +11,28 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaw.so")
+# AW_DEV_BUILD=1: development build -- adds the measurement variants of the streaming kernel
+# (aw_stream_r{4,6,8}v.cu, AW_STREAM_VARIANT) and makes libaw read the development knobs
+# (aw_internal.h dev_knob).  The product library (default) has neither.
+DEV = os.environ.get("AW_DEV_BUILD", "0") == "1"
 SOURCES = (["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu", "aw_fwi.cu", "aw_stencil2d.cu"]
-           + [f"aw_stream_r{r}.cu" for r in range(1, 9)] + ["aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"])
+           + [f"aw_stream_r{r}.cu" for r in range(1, 9)]
+           + (["aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"] if DEV else []))
 HEADERS = ["aw_internal.h", "aw_stream.cuh", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-v", "-I" + os.path.join(HERE, "..", "include")]
+if DEV:
+    FLAGS += ["-DAW_DEV_KNOBS", "-DAW_DEV_VARIANTS"]
+STAMP = os.path.join(CSRC, ".build_kind")  # "dev" / "product": a switch forces a rebuild
 
 
 def _stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    kind = "dev" if DEV else "product"
+    if not os.path.exists(STAMP) or open(STAMP).read().strip() != kind:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]
@@ -52,6 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write("dev" if DEV else "product")
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:

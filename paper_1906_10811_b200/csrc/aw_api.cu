@@ -550,7 +550,7 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0
     }
     if (e0) CK(cudaEventRecord(e0, g->s));
     // receivers + injection inside the stencil kernel (AW_NO_FUSE=1: separate sparse kernel, for A/B runs)
-    static const bool no_fuse = getenv("AW_NO_FUSE") != nullptr;
+    static const bool no_fuse = aw::dev_knob("AW_NO_FUSE") != nullptr;
     const bool fused = g->kernel_used == AW_KERNEL_STREAM && !no_fuse;
     if (g->kernel_used == AW_KERNEL_STREAM) {
         aw::Sparse sp = sparse_view(g);
@@ -674,7 +674,7 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
         }
     }
     g->n_timed = timing ? nt : 0;
-    static const bool no_fuse = getenv("AW_NO_FUSE") != nullptr;
+    static const bool no_fuse = aw::dev_knob("AW_NO_FUSE") != nullptr;
     if (g->tb_ready && !team_mode(g) && !no_fuse && nt >= 2) {
         // NEXT-1: two steps per launch over three rotating buffers (direct launches, one per pass)
         const float* a = g->have_damp ? g->a : nullptr;
@@ -1188,7 +1188,16 @@ aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, 
     for (int which = 0; which < 2; ++which) {
         float* buf = g->ubuf[which == 0 ? g->cur : 1 - g->cur];
         const float* src = which == 0 ? u_cur : u_prev;
-        CK(cudaMemsetAsync(buf, 0, g->ubytes, g->s));
+        {
+            // LOCAL in a team: the neighbours fill my halo planes next to them (their prologue copy at
+            // the next run may land before or after this call), so leave those planes alone and zero
+            // the rest (owned planes, the always-zero halo at a global end).  GLOBAL: every rank fills
+            // its own halos from the global array below (or zeros).
+            const bool local_team = team_mode(g) && layout == AW_LOCAL;
+            const int64_t zb = local_team && g->halo.lo[0] ? 0 : -R;
+            const int64_t ze = local_team && g->halo.hi[0] ? nz : nz + R;
+            CK(cudaMemsetAsync(buf + (zb + R) * plane, 0, (size_t)(ze - zb) * plane * sizeof(float), g->s));
+        }
         if (!src) continue;
         int64_t zlo = 0, zhi = nz;  // local planes to fill
         if (layout == AW_GLOBAL && which == 0 && team_mode(g)) {

@@ -3,11 +3,24 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #define AW_MAXR 8          // space order <= 16
 #define AW_PITCH_ALIGN 32  // x pitch in floats (128 B rows: coalescing + TMA 16-B strides)
 
 namespace aw {
+
+// Development knobs (environment variables for A/B measurements: AW_STREAM_VARIANT, AW_STREAM_ZC,
+// AW_TB_Z, AW_TB_LEAD, AW_NO_FUSE).  Read only in development builds (AW_DEV_BUILD=1 ->
+// -DAW_DEV_KNOBS); the product library ignores them.
+inline const char* dev_knob(const char* name) {
+#ifdef AW_DEV_KNOBS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 // Axis coefficients of the star Laplacian, fp32:
 // C[d][j] = fl32(c_j / h_d^2), C0 = fl32(sum_d c_0 / h_d^2).

@@ -73,7 +73,7 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     const int ntiles = p->ntx * p->nty;
     int nzc = 1;
     while ((int64_t)ntiles * nzc < 8LL * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
-    if (const char* zc_env = getenv("AW_STREAM_ZC")) {  // development knob: planes per z chunk
+    if (const char* zc_env = dev_knob("AW_STREAM_ZC")) {  // development knob: planes per z chunk
         const int zc = atoi(zc_env);
         if (zc > 0) nzc = (g.nz + zc - 1) / zc;
     }
@@ -211,13 +211,13 @@ cudaError_t launch_stencil_stream_bufs(StreamPlan* p, const Geom& g, const Coefs
 cudaError_t stream_tb_prepare(StreamPlan* p, const Geom& g, int Z) {
     if (!p) return cudaErrorNotSupported;
     if (Z <= 0) Z = 32;  // best of 8/16/24/32/48/64 on C3 (profiles/r1/tb_sweep.jsonl)
-    if (const char* z_env = getenv("AW_TB_Z")) {  // development knob
+    if (const char* z_env = dev_knob("AW_TB_Z")) {  // development knob
         const int z = atoi(z_env);
         if (z > 0) Z = z;
     }
     if (Z < 2 * g.R) Z = 2 * g.R;
     int lead = 2;  // A phases handed out ahead of the first B phase (>= 1: B(c) must follow A(c))
-    if (const char* l_env = getenv("AW_TB_LEAD")) lead = atoi(l_env) > 1 ? atoi(l_env) : 1;
+    if (const char* l_env = dev_knob("AW_TB_LEAD")) lead = atoi(l_env) > 1 ? atoi(l_env) : 1;
     p->tb_lead = lead;
     const int nzc = (g.nz + Z - 1) / Z;
     const int64_t n = (int64_t)nzc * p->ntx * p->nty;

@@ -371,16 +371,25 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                         }
                     }
                 }
-                if (TEAM && ((A.lo && z < R) || (A.hi && z >= nz - R))) {
-                    // fused exchange: boundary planes also go straight into the neighbour's halo
+                if constexpr (TEAM) {
+                    // fused exchange: boundary planes also go straight into the neighbours' halos.  A plane
+                    // of a thin slab (R <= nz < 2R) can be both a low and a high boundary plane, so the
+                    // two targets are tested separately.
                     const int64_t om = (outp - out_base) - (int64_t)R * plane;  // model-layout index
-                    float* h = (A.lo && z < R) ? A.lo + A.lo_off + om
-                                               : A.hi + A.hi_off + om - (int64_t)(nz - R) * plane;
+                    auto peer_store = [&](float* h) {
 #pragma unroll
-                    for (int i = 0; i < RY; ++i) {
-                        if (ok_a[i]) h[i * pitch] = res[i].x;
-                        if (ok_b[i]) h[i * pitch + CB] = res[i].y;
-                    }
+                        for (int i = 0; i < RY; ++i) {
+                            float* o = h + i * pitch;
+                            if (C::ADJ && ok_a[i] && ok_b[i]) {
+                                *reinterpret_cast<float2*>(o) = res[i];  // same pitch and alignment as outp
+                            } else {
+                                if (ok_a[i]) o[0] = res[i].x;
+                                if (ok_b[i]) o[CB] = res[i].y;
+                            }
+                        }
+                    };
+                    if (A.lo && z < R) peer_store(A.lo + A.lo_off + om);
+                    if (A.hi && z >= nz - R) peer_store(A.hi + A.hi_off + om - (int64_t)(nz - R) * plane);
                 }
                 outp += plane;
             }
@@ -1032,7 +1041,7 @@ using C8v2 = Cfg<8, 16, 1, 4, 4, 0, 1>;  // 16 consumer warps, one row each
 using C8v3 = Cfg<8, 16, 2, 4, 4, 0, 1, false>;
 
 int variant() {
-    const char* v = getenv("AW_STREAM_VARIANT");
+    const char* v = dev_knob("AW_STREAM_VARIANT");
     return v ? atoi(v) : 0;
 }
 

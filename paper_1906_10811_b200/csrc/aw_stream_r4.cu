@@ -2,10 +2,14 @@
 #include "aw_stream.cuh"
 
 namespace aw {
-const StreamOps* stream_ops_r4_variant(int v);  // aw_stream_r4v.cu (development variants)
+#ifdef AW_DEV_VARIANTS
+const StreamOps* stream_ops_r4_variant(int v);  // aw_stream_r4v.cu (development variants, dev builds only)
+#endif
 
 const StreamOps* stream_ops_r4() {
-    const int v = variant();  // AW_STREAM_VARIANT=1/2/3: measurement variants of the R=4 configuration
-    return v ? stream_ops_r4_variant(v) : ops_of<C4>();
+#ifdef AW_DEV_VARIANTS
+    if (const int v = variant()) return stream_ops_r4_variant(v);  // AW_STREAM_VARIANT=1/2/3 (A/B measurements)
+#endif
+    return ops_of<C4>();
 }
 }  // namespace aw

@@ -2,10 +2,14 @@
 #include "aw_stream.cuh"
 
 namespace aw {
-const StreamOps* stream_ops_r8_variant(int v);  // aw_stream_r8v.cu (measurement variants)
+#ifdef AW_DEV_VARIANTS
+const StreamOps* stream_ops_r8_variant(int v);  // aw_stream_r8v.cu (measurement variants, dev builds only)
+#endif
 
 const StreamOps* stream_ops_r8() {
-    const int v = variant();
-    return v ? stream_ops_r8_variant(v) : ops_of<C8>();
+#ifdef AW_DEV_VARIANTS
+    if (const int v = variant()) return stream_ops_r8_variant(v);  // AW_STREAM_VARIANT=1/2/3 (A/B measurements)
+#endif
+    return ops_of<C8>();
 }
 }  // namespace aw

@@ -89,13 +89,13 @@ def _allreduce(grad, J: float, group=None):
         return grad, J
     import torch
     backend = dist.get_backend(group)
-    if hasattr(grad, "data_ptr"):
-        t = grad if (backend == "nccl" or not grad.is_cuda) else grad.cpu()
-    else:
-        t = torch.from_numpy(grad)
+    # NCCL reduces device tensors only; gloo host tensors only: stage through the right side
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    src = grad if hasattr(grad, "data_ptr") else torch.from_numpy(grad)
+    t = src if src.device == dev else src.to(dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    if hasattr(grad, "data_ptr") and t is not grad:
-        grad.copy_(t)
+    if t is not src:
+        src.copy_(t)  # numpy grad: src shares its memory
     jt = torch.tensor([J], dtype=torch.float64, device=t.device)
     dist.all_reduce(jt, op=dist.ReduceOp.SUM, group=group)
     return grad, float(jt.item())

@@ -290,3 +290,64 @@ def test_virtual_team_equals_single(aw, world, ndim):
     ou, _, orec = run_oracle(w)
     assert_parity(u, ou, "team u")
     assert_parity(rec, orec, "team traces")
+
+
+@pytest.mark.parametrize("kernel", ["auto", "v1"])
+def test_virtual_team_thin_slabs(aw, kernel):
+    """Slabs thinner than 2R (R <= nz < 2R): a middle rank's planes are both low and high boundary
+    planes and must reach BOTH neighbours' halos (fused stores of the streaming kernel and v1)."""
+    k, world = 8, 3
+    w = workloads.small_case((18, 29, 70), k, 24, nbl=3, ns=2, nr=6, seed=31)
+    assert all(4 <= aw.slab_partition(18, world, r, k // 2)[1] < 8 for r in range(world))
+    grids = [aw.Grid(w.shape, w.extent, k, rank=r, world=world) for r in range(world)]
+    aw.team_connect_local(grids)
+    for g in grids:
+        if kernel == "v1":
+            g.set_option(aw.AW_OPT_KERNEL, aw.AW_KERNEL_V1)
+        g.set_model(w.m, w.damp)
+        g.add_sources(w.src_coords, w.wavelet)
+        g.add_receivers(w.rec_coords, w.nt)
+    aw.team_run(grids, w.nt, w.dt)
+    u = np.zeros(w.shape, np.float32)
+    rec = np.zeros((w.nt, len(w.rec_coords)), np.float32)
+    for g in grids:
+        g.read_wavefield(0, out=u)
+        rec += g.read_receivers()
+        g.close()
+    ou, _, orec = run_oracle(w)
+    assert_parity(u, ou, "thin-slab team u")
+    assert_parity(rec, orec, "thin-slab team traces")
+
+
+def test_virtual_team_local_restart(aw):
+    """Restart of a team from per-rank (AW_LOCAL) wavefields: run a steps, read each rank's slab of
+    both levels, set them into a fresh team (halo exchange at the next run), run b more steps
+    == one run of a+b (the oracle), bit-exact."""
+    k, world, a_steps = 8, 3, 10
+    w = workloads.small_case((40, 29, 70), k, 26, nbl=3, ns=1, nr=5, seed=33)
+    w.rec_coords = np.zeros((0, 3))
+
+    first = [aw.Grid(w.shape, w.extent, k, rank=r, world=world) for r in range(world)]
+    aw.team_connect_local(first)
+    for g in first:
+        g.set_model(w.m, w.damp)
+        g.add_sources(w.src_coords, w.wavelet)
+    aw.team_run(first, a_steps, w.dt)
+    levels = [(g.read_wavefield(0, layout=aw.AW_LOCAL), g.read_wavefield(1, layout=aw.AW_LOCAL)) for g in first]
+    for g in first:
+        g.close()
+    # the fresh team starts its step counter at 0: its wavelet rows start at global step a_steps
+    shifted = w.wavelet[a_steps:].copy()
+    second = [aw.Grid(w.shape, w.extent, k, rank=r, world=world) for r in range(world)]
+    aw.team_connect_local(second)
+    for g, (uc, up) in zip(second, levels):
+        g.set_model(w.m, w.damp)
+        g.add_sources(w.src_coords, shifted)
+        g.set_wavefield(uc, up, layout=aw.AW_LOCAL)
+    aw.team_run(second, w.nt - a_steps, w.dt)
+    u = np.zeros(w.shape, np.float32)
+    for g in second:
+        g.read_wavefield(0, out=u)
+        g.close()
+    ou, _, _ = run_oracle(w)
+    assert_parity(u, ou, "team LOCAL restart u")
