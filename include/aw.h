@@ -46,7 +46,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define AW_ABI_VERSION 1
+#define AW_ABI_VERSION 2
 
 typedef struct aw_grid aw_grid; /* opaque; created by aw_grid_create, freed by aw_grid_destroy */
 
@@ -85,12 +85,17 @@ enum {
                            set; setting it (either value) clears the sum.  J is still per call. */
 };
 
+/* aw_dist.flags */
+enum { AW_DIST_WORKSPACE = 1 /* the caller provides the device memory of the grid's arrays with
+                               aw_bind_workspace: aw_grid_create allocates none of them */ };
+
 /* multi-rank description: one process (or virtual rank) per slab of axis 0 */
 typedef struct {
     int rank;       /* 0 <= rank < world */
     int world;      /* number of slabs along axis 0 (1 = single GPU) */
     int device;     /* CUDA device ordinal to use (-1 = current device) */
     void* stream;   /* cudaStream_t to launch on (NULL = library-owned stream) */
+    unsigned flags; /* AW_DIST_* bits (0 = library-allocated arrays) */
 } aw_dist;
 
 /*
@@ -104,7 +109,12 @@ typedef struct {
  *   dist         NULL = one slab on the current device; otherwise the slab
  *                [z0, z0+nz) of axis 0 owned by dist->rank (nearly equal split)
  * Device memory: 2 wavefield levels with k/2 halo planes on each side of
- * axis 0 plus b, a, m, eta per owned point (fp32, x pitch padded to 128 B).
+ * axis 0 plus b, a, m, eta per owned point (fp32, x pitch padded to 128 B),
+ * zero-filled ("zero-filled buffer ... allocation failure
+ * surfaced as resource error" -> AW_ENOMEM).  With dist->flags &
+ * AW_DIST_WORKSPACE none of these arrays is allocated: the caller binds the
+ * memory with aw_bind_workspace before any call that touches them (those calls
+ * return AW_ESTATE until then).
  */
 aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const double* extent,
                          const double* origin, int space_order, const aw_dist* dist);
@@ -112,7 +122,33 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
 /* NULL-safe; never fails.  Must not be called while another rank of a team still runs. */
 void aw_grid_destroy(aw_grid* g);
 
-/* This handle's slab of axis 0: planes [*z0, *z0 + *nz). */
+/*
+ * aw_workspace_bytes -- bytes of device memory the grid's arrays need in a
+ * caller-owned workspace (the north star's "PyTorch only for device memory",
+ * BASELINE.json:5): the two wavefield levels, m, eta, b, a
+ * (the dense part, fixed by the grid) plus the sparse arenas of the sources
+ * and receivers added so far (call after aw_add_sources/aw_add_receivers to
+ * include them).  0 for a NULL handle.
+ *
+ * aw_bind_workspace -- hand the library `bytes` bytes of device memory at
+ * dev_ptr (on the grid's device, 256-B aligned, e.g. a torch uint8 tensor).
+ * The dense arrays move into [0, dense) (contents copied if they already held
+ * data; the library's own allocation is freed), and the rest of the workspace
+ * holds the source arena, then the receiver arena; an arena that outgrows its
+ * slot later falls back to a library allocation (reported in
+ * aw_run_stats.lib_device_bytes).  The workspace is BORROWED: it must stay
+ * allocated and untouched until aw_grid_destroy or the next bind.  Must be
+ * called before a team connects (peers hold the wavefield addresses).
+ * Errors: AW_EINVAL (NULL/unaligned pointer, bytes < the dense part, memory on
+ * another device), AW_ESTATE (team already connected).  The handle is
+ * unchanged on error.
+ */
+size_t aw_workspace_bytes(const aw_grid* g);
+aw_status aw_bind_workspace(aw_grid* g, void* dev_ptr, size_t bytes);
+
+/* This handle's slab of axis 0: planes [*z0, *z0 + *nz) (nearly
+ * equal slabs of the slowest axis; "MPI ... domain partitioning"
+ * as an OPS capability).  Either output may be NULL. */
 aw_status aw_local_extent(const aw_grid* g, int64_t* z0, int64_t* nz);
 
 /*
@@ -121,7 +157,8 @@ aw_status aw_local_extent(const aw_grid* g, int64_t* z0, int64_t* nz);
  * (AW_GLOBAL) or this rank's slab (AW_LOCAL).  The dt-dependent coefficients
  * b = fl32(dt^2/m), a = fl32(m/(m + eta dt/2)) (the paper's
  * division hoisting PAPER.md:788-792) are (re)computed on the device at the
- * next aw_run.  Invalid values -> AW_EINVAL (checked on the device).
+ * next aw_run.  Invalid values -> AW_EINVAL (checked on the device, on a
+ * staged copy: the previous model stays in force, strong guarantee).
  */
 aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout);
 
@@ -146,7 +183,11 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
 
 /*
  * aw_set_wavefield -- initial conditions / restart: u_cur = u^{n}, u_prev =
- * u^{n-1} (fp32 [H|D], NULL = zeros) for the current step counter.
+ * u^{n-1} (fp32 [H|D], NULL = zeros) for the current step counter (the two
+ * levels of the leapfrog; SPEC.md:352/:639 restart ==
+ * continuous run).  In a team the call is collective: every rank calls it
+ * with the same layout after all ranks' previous aw_run returned (a barrier);
+ * with AW_LOCAL the halo planes are exchanged at the next aw_run.
  */
 aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, int layout);
 
@@ -160,7 +201,10 @@ aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, 
  */
 aw_status aw_run(aw_grid* g, int nt, double dt);
 
-/* Zero both wavefield levels and the traces, reset the step counter and dt. */
+/* Zero both wavefield levels and the traces, reset the step counter and dt:
+ * back to the zero-filled state of creation (PAPER.md:455-491 zero padding,
+ * SPEC.md:68-76; SURVEY §8(c).5 "u^0 = u^-1 = 0").  In a team the call is
+ * collective and needs a barrier before it, as aw_set_wavefield. */
 aw_status aw_reset(aw_grid* g);
 
 /* Number of steps taken since create/reset. */
@@ -169,7 +213,9 @@ int64_t aw_steps_done(const aw_grid* g);
 /*
  * aw_read_wavefield -- copy u^{n} (which = 0, the newest level) or u^{n-1}
  * (which = 1) into out (fp32 [H|D], dense, global or local layout; a rank
- * asked for AW_GLOBAL writes only its own planes of the global array).
+ * asked for AW_GLOBAL writes only its own planes of the global array).  The
+ * output of SURVEY §8(c).7 ("read_wavefield(0) = u^{n0+nt}"); the paper's
+ * time-buffer rotation t_k = (time+k) mod n is internal.
  */
 aw_status aw_read_wavefield(aw_grid* g, int which, float* out, int layout);
 
@@ -202,6 +248,12 @@ typedef struct {
     int fwi_checkpoint;   /* checkpoint segment length K used by the last aw_fwi_gradient */
     int64_t timed_launches; /* stencil launches timed by the last aw_run (AW_OPT_TIMING; a temporal-
                                blocking pass covers two of the n_stencil steps) */
+    double ms_exchange;   /* team: time the last aw_run's boundary work waited for the neighbours' halo
+                             planes (device clock, summed over steps of the per-step mean wait of the
+                             waiting CTAs; 0 for a single slab) -- SURVEY §5 tracing row, §8(e) */
+    int64_t exchange_waits; /* team: waits that found the neighbour's halo not yet delivered */
+    int64_t lib_device_bytes; /* device bytes the library itself holds for this handle (cudaMalloc) */
+    int64_t workspace_bytes;  /* bytes of the bound caller workspace (0 = none) */
 } aw_run_stats;
 
 aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out);

@@ -31,20 +31,23 @@ AW_GLOBAL, AW_LOCAL = 0, 1
 AW_KERNEL_AUTO, AW_KERNEL_V1, AW_KERNEL_STREAM, AW_KERNEL_TILE2D = 0, 1, 2, 3
 AW_OPT_KERNEL, AW_OPT_TIMING, AW_OPT_GRAPH_STEPS, AW_OPT_CHECK_FINITE, AW_OPT_CHECKPOINT_STEPS = 1, 2, 3, 4, 5
 AW_OPT_TEMPORAL, AW_OPT_FWI_ACCUMULATE = 6, 7
+AW_DIST_WORKSPACE = 1
 STATUS_NAMES = {0: "AW_OK", -1: "AW_EINVAL", -2: "AW_ENOMEM", -3: "AW_ECUDA", -4: "AW_ENCCL",
                 -5: "AW_ESTATE", -6: "AW_EUNSUPPORTED", -7: "AW_ENONFINITE"}
 
 
 class aw_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("flags", ctypes.c_uint)]
 
 
 class aw_run_stats(ctypes.Structure):
     _fields_ = [("ms_total", ctypes.c_double), ("ms_stencil", ctypes.c_double), ("n_stencil", ctypes.c_int64),
                 ("launches", ctypes.c_int64), ("gpts", ctypes.c_double), ("points", ctypes.c_int64),
                 ("kernel", ctypes.c_int), ("eta_tiles", ctypes.c_int), ("launches_total", ctypes.c_int64),
-                ("fwi_steps", ctypes.c_int64), ("fwi_checkpoint", ctypes.c_int), ("timed_launches", ctypes.c_int64)]
+                ("fwi_steps", ctypes.c_int64), ("fwi_checkpoint", ctypes.c_int), ("timed_launches", ctypes.c_int64),
+                ("ms_exchange", ctypes.c_double), ("exchange_waits", ctypes.c_int64),
+                ("lib_device_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p
@@ -57,6 +60,8 @@ _SIGS = {
     "aw_grid_create": (_S, [ctypes.POINTER(_P), _I, _P, _P, _P, _I, ctypes.POINTER(aw_dist)]),
     "aw_grid_destroy": (None, [_P]),
     "aw_local_extent": (_S, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "aw_workspace_bytes": (ctypes.c_size_t, [_P]),
+    "aw_bind_workspace": (_S, [_P, _P, ctypes.c_size_t]),
     "aw_set_model": (_S, [_P, _P, _P, _I]),
     "aw_add_sources": (_S, [_P, _I, _P, _I, _P]),
     "aw_add_receivers": (_S, [_P, _I, _P, _I]),
@@ -152,7 +157,11 @@ def _torch_stream_handle(stream):
 class Grid:
     """Owner of one ``aw_grid*`` (one slab / one GPU)."""
 
-    def __init__(self, shape, extent, space_order, origin=None, *, rank=0, world=1, device=None, stream=None):
+    def __init__(self, shape, extent, space_order, origin=None, *, rank=0, world=1, device=None, stream=None,
+                 workspace=None):
+        """workspace: None = the library allocates the grid arrays; "defer" = allocate nothing now
+        (AW_DIST_WORKSPACE; call bind_workspace before set_model/run); a torch uint8 CUDA tensor =
+        bind it right away (torch owns the device memory, include/aw.h aw_bind_workspace)."""
         self.ndim = len(shape)
         self.shape = tuple(int(s) for s in shape)
         sh = (ctypes.c_int64 * self.ndim)(*self.shape)
@@ -160,7 +169,8 @@ class Grid:
         org = None if origin is None else (ctypes.c_double * self.ndim)(*[float(o) for o in origin])
         if stream is not None and not isinstance(stream, int):
             stream = _torch_stream_handle(stream)
-        dist = aw_dist(rank, world, -1 if device is None else int(device), stream)
+        flags = 0 if workspace is None else AW_DIST_WORKSPACE
+        dist = aw_dist(rank, world, -1 if device is None else int(device), stream, flags)
         h = _P()
         check(aw_grid_create(ctypes.byref(h), self.ndim, ctypes.cast(sh, _P), ctypes.cast(ex, _P),
                              None if org is None else ctypes.cast(org, _P), int(space_order), ctypes.byref(dist)))
@@ -172,12 +182,36 @@ class Grid:
         self.z0, self.nz = z0.value, nz.value
         self.nr = 0
         self.ns = 0
+        self.device = device
+        self._ws = None
+        if workspace is not None and not isinstance(workspace, str):
+            self.bind_workspace(workspace)
+        elif workspace not in (None, "defer"):
+            raise ValueError("workspace must be None, 'defer' or a torch uint8 CUDA tensor")
+
+    def workspace_bytes(self) -> int:
+        """Bytes a caller workspace needs now (grid arrays + current sparse arenas)."""
+        return int(aw_workspace_bytes(self.handle))
+
+    def bind_workspace(self, ws=None, extra: int = 0):
+        """Bind a torch uint8 CUDA tensor as the grid's device memory (allocated here with
+        workspace_bytes() + extra bytes when ws is None).  The tensor is kept alive by the Grid."""
+        import torch
+        if ws is None:
+            dev = torch.device("cuda", torch.cuda.current_device() if self.device is None else int(self.device))
+            ws = torch.empty(self.workspace_bytes() + int(extra), dtype=torch.uint8, device=dev)
+        if not (hasattr(ws, "data_ptr") and ws.dtype == torch.uint8 and ws.is_cuda and ws.is_contiguous()):
+            raise TypeError("workspace must be a contiguous torch.uint8 CUDA tensor")
+        check(aw_bind_workspace(self.handle, ws.data_ptr(), ws.numel()))
+        self._ws = ws
+        return ws
 
     # lifecycle
     def close(self):
         if getattr(self, "handle", None):
             aw_grid_destroy(self.handle)
             self.handle = None
+        self._ws = None  # the library no longer references the workspace
 
     def __del__(self):
         try:

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/aw.h"
@@ -114,14 +115,24 @@ struct aw_grid {
     cudaStream_t ext = nullptr;
     cudaEvent_t ev_sync = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
     bool poisoned = false;
-    // device memory
+    // device memory.  The dense arrays (2 wavefield levels, m, eta, b, a) live in one block: the
+    // library's own allocation (dense_lib) or the caller's workspace (aw_bind_workspace).
     float* ubuf[2] = {nullptr, nullptr};
     size_t ubytes = 0;  // per wavefield buffer
     float *m = nullptr, *eta = nullptr, *b = nullptr, *a = nullptr;
     size_t mbytes = 0;
-    int64_t* d_base = nullptr;
-    unsigned* d_flag = nullptr;
-    unsigned long long* d_team_flags = nullptr;  // [2]: from rank-1, from rank+1
+    char* dense = nullptr;      // block in use (nullptr: AW_DIST_WORKSPACE and nothing bound yet)
+    char* dense_lib = nullptr;  // the library's block (freed when a workspace is bound)
+    size_t dense_bytes = 0;
+    char* ws = nullptr;         // bound caller workspace
+    size_t ws_bytes = 0;
+    size_t ws_slot_off[2] = {0, 0}, ws_slot_cap[2] = {0, 0};  // sparse arena slots: [0] sources, [1] receivers
+    size_t src_need = 0, rec_need = 0;                         // bytes of the current sparse arenas
+    std::map<void*, size_t> lib_allocs;                        // the library's own device allocations
+    aw::DevCtl* ctl = nullptr;  // device control block (step base, epoch, flags, team words)
+    int64_t* d_base = nullptr;  // &ctl->base
+    unsigned* d_flag = nullptr; // &ctl->flag
+    unsigned long long* d_team_flags = nullptr;  // ctl->team_flags: [0] from rank-1, [1] from rank+1
     // state
     bool have_model = false, have_damp = false, coeffs_valid = false, dt_set = false;
     double dt = 0.0;
@@ -171,6 +182,7 @@ struct aw_grid {
     unsigned long long* peer_flag_lo = nullptr;  // &flags_{rank-1}[1]
     unsigned long long* peer_flag_hi = nullptr;  // &flags_{rank+1}[0]
     std::vector<void*> ipc_opened;
+    std::vector<std::pair<cudaIpcMemHandle_t, void*>> ipc_opened_h;
     bool team_connected = false;
     bool halo_dirty = false;  // LOCAL set_wavefield in a team: exchange before the next run
     int64_t nz_lo = 0;
@@ -237,11 +249,24 @@ void free_graphs(aw_grid* g) {
     g->graphs.clear();
 }
 
+// The library's own device allocations are tracked (aw_run_stats.lib_device_bytes).
+cudaError_t lmalloc(aw_grid* g, void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) g->lib_allocs[*p] = bytes;
+    return e;
+}
+bool in_ws(const aw_grid* g, const void* p) {
+    return g->ws && p >= (const void*)g->ws && p < (const void*)(g->ws + g->ws_bytes);
+}
 template <class T>
-void dfree(T*& p) {
-    if (p) cudaFree((void*)p);
+void dfree(aw_grid* g, T*& p) {  // frees library memory only (never a pointer into the workspace)
+    if (p && !in_ws(g, p)) {
+        cudaFree((void*)p);
+        g->lib_allocs.erase((void*)p);
+    }
     p = nullptr;
 }
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Synchronise the library stream with the caller's stream (entry) ...
 aw_status enter(aw_grid* g) {
@@ -380,6 +405,26 @@ void build_injection(const aw_grid* g, int n, const std::vector<int64_t>& corner
     t->ptr.push_back((int)ents.size());
 }
 
+// The dense block: u^a, u^b (wavefield layout, planes [-R, nz+R)), then four model-layout arrays
+// (m, eta, b, a).  aw_set_model swaps the roles of m<->b and eta<->a (staging), so after the first
+// placement the pointers, not the offsets, say which array is which.
+constexpr size_t kDenseAlign = 4096;
+void place_dense(aw_grid* g, char* base) {
+    const size_t U = align_up(g->ubytes, kDenseAlign), M = align_up(g->mbytes, kDenseAlign);
+    g->dense = base;
+    g->ubuf[0] = (float*)base;
+    g->ubuf[1] = (float*)(base + U);
+    g->m = (float*)(base + 2 * U);
+    g->eta = (float*)(base + 2 * U + M);
+    g->b = (float*)(base + 2 * U + 2 * M);
+    g->a = (float*)(base + 2 * U + 3 * M);
+}
+#define NEED_DENSE(g)                                                                                   \
+    do {                                                                                                \
+        if (!(g)->dense) return fail(AW_ESTATE, "no device memory bound yet (AW_DIST_WORKSPACE): call "   \
+                                                "aw_bind_workspace first");                             \
+    } while (0)
+
 unsigned long long enc(const aw_grid* g, int64_t level) {
     return (g->epoch << 32) + (unsigned long long)(level + 1);
 }
@@ -395,6 +440,7 @@ void free_sources(aw_grid* g) {  // the device arrays are views into g->src_aren
     g->d_inj_w64 = nullptr;
     g->d_inj_s = nullptr;
     g->ns = g->src_nt = g->nuc = g->nent = 0;
+    g->src_need = 0;
     g->src_corner_lin.clear();
     g->src_w64.clear();
     g->ent_src.clear();
@@ -408,19 +454,11 @@ void free_receivers(aw_grid* g) {  // views into g->rec_arena
     g->d_rec_w = nullptr;
     g->d_traces = nullptr;
     g->nr = g->rec_nt = g->nrl = 0;
+    g->rec_need = 0;
     g->rec_corner_lin.clear();
     g->rec_w32.clear();
     g->rec_w64.clear();
     g->adj_valid = false;
-}
-
-template <class T>
-aw_status upload(aw_grid* g, T** dst, const std::vector<T>& v) {
-    dfree(*dst);
-    if (v.empty()) return AW_OK;
-    CK(cudaMalloc((void**)dst, v.size() * sizeof(T)));
-    CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, g->s));
-    return AW_OK;
 }
 
 // Packs several host arrays into one device arena (16-B aligned slices) with a single copy.
@@ -442,16 +480,30 @@ struct Packer {
     }
 };
 
-aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes) {
+// slot: 0 = the sources' arena, 1 = the receivers' (placed in the bound workspace when they fit),
+// -1 = an arena that always lives in library memory (FWI)
+aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes, int slot = -1) {
+    if (slot >= 0 && g->ws && g->ws_slot_cap[slot] >= bytes) {
+        char* w = g->ws + g->ws_slot_off[slot];
+        if (*arena != w) {
+            if (*arena && !in_ws(g, *arena)) {
+                CK(cudaStreamSynchronize(g->s));
+                dfree(g, *arena);
+            }
+            *arena = w;
+            *cap = g->ws_slot_cap[slot];
+        }
+        return AW_OK;
+    }
     if (*cap >= bytes && *arena) return AW_OK;
     if (*arena) {
         CK(cudaStreamSynchronize(g->s));
-        cudaFree(*arena);
+        dfree(g, *arena);
         *arena = nullptr;
         *cap = 0;
     }
     size_t want = bytes + bytes / 2 + 256;
-    cudaError_t e = cudaMalloc((void**)arena, want);
+    cudaError_t e = lmalloc(g, (void**)arena, want);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(e == cudaErrorMemoryAllocation ? AW_ENOMEM : AW_ECUDA, "sparse arena: %s", cudaGetErrorString(e));
@@ -512,7 +564,7 @@ aw_status prepare(aw_grid* g, double dt) {
             g->tb_ready = false;
             if (g->opt_temporal && !team_mode(g)) {
                 if (!g->ubuf_spare) {
-                    CK(cudaMalloc((void**)&g->ubuf_spare, g->ubytes));
+                    CK(lmalloc(g, (void**)&g->ubuf_spare, g->ubytes));
                     CK(cudaMemsetAsync(g->ubuf_spare, 0, g->ubytes, g->s));  // zero halo planes for good
                 }
                 CK(aw::stream_tb_prepare(g->plan, g->geom, 0));
@@ -540,12 +592,11 @@ aw_status prepare(aw_grid* g, double dt) {
 
 // Enqueue one time step (local index i relative to *d_base) reading buffer
 // `cur` (u^n) and writing buffer 1-cur (u^{n+1} over u^{n-1}).
-aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0, cudaEvent_t e1, int64_t* launches) {
+aw_status enqueue_step(aw_grid* g, int i, int cur, cudaEvent_t e0, cudaEvent_t e1, int64_t* launches) {
     const int nxt = 1 - cur;
     if (team_mode(g)) {
-        unsigned long long want_lo = g->halo.lo[0] ? enc(g, level) : 0ull;
-        unsigned long long want_hi = g->halo.hi[0] ? enc(g, level) : 0ull;
-        CK(aw::launch_team_wait(g->d_team_flags, want_lo, want_hi, g->s));
+        // the wanted level comes from the device (step base + i, epoch): graph-capturable
+        CK(aw::launch_team_wait(g->ctl, g->halo.lo[0] != nullptr, g->halo.hi[0] != nullptr, i, g->s));
         ++*launches;
     }
     if (e0) CK(cudaEventRecord(e0, g->s));
@@ -573,7 +624,7 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, int64_t level, cudaEvent_t e0
         ++*launches;
     }
     if (team_mode(g) && (g->peer_flag_lo || g->peer_flag_hi)) {
-        CK(aw::launch_team_signal(g->peer_flag_lo, g->peer_flag_hi, g->epoch << 32, g->d_base, i, g->s));
+        CK(aw::launch_team_signal(g->peer_flag_lo, g->peer_flag_hi, g->ctl, i, g->s));
         ++*launches;
     }
     return AW_OK;
@@ -592,7 +643,7 @@ aw_status get_graph(aw_grid* g, int G, int cur, cudaGraphExec_t* out) {
     int c = cur;
     aw_status st = AW_OK;
     for (int i = 0; i < G && st == AW_OK; ++i) {
-        st = enqueue_step(g, i, c, 0, nullptr, nullptr, &dummy);
+        st = enqueue_step(g, i, c, nullptr, nullptr, &dummy);
         c = 1 - c;
     }
     if (st == AW_OK) {
@@ -645,6 +696,7 @@ aw_status team_prologue(aw_grid* g) {
 }
 
 aw_status run_begin(aw_grid* g, int nt, double dt) {
+    NEED_DENSE(g);
     aw_status st = check_run_args(g, nt, dt);
     if (st) return st;
     if (team_mode(g) && !g->team_connected) return fail(AW_ESTATE, "team handle is not connected");
@@ -658,6 +710,7 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
     int64_t base = g->steps;
     CK(cudaMemcpyAsync(g->d_base, &base, sizeof base, cudaMemcpyHostToDevice, g->s));
     CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
+    CK(cudaMemsetAsync(&g->ctl->wait_ns, 0, 2 * sizeof(unsigned long long), g->s));  // wait_ns, nwait
     return AW_OK;
 }
 
@@ -711,13 +764,15 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
         return AW_OK;
     }
     int done = 0;
-    if (!timing && !team_mode(g) && G > 0) {
+    if (!timing && G > 0) {  // team steps too: their waits and signals read the level from the device
         while (nt - done >= G) {
             cudaGraphExec_t exec;
             aw_status st = get_graph(g, G, g->cur, &exec);
             if (st) return st;
             CK(cudaGraphLaunch(exec, g->s));
-            *launches += (int64_t)G * (1 + (g->kernel_used != AW_KERNEL_STREAM && g->nrl + g->nuc > 0 ? 1 : 0)) + 1;
+            const int per_step = 1 + (g->kernel_used != AW_KERNEL_STREAM && g->nrl + g->nuc > 0 ? 1 : 0) +
+                                 (team_mode(g) ? 1 + (g->peer_flag_lo || g->peer_flag_hi ? 1 : 0) : 0);
+            *launches += (int64_t)G * per_step + 1;
             done += G;
             if (G & 1) g->cur = 1 - g->cur;
         }
@@ -726,7 +781,7 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
     const int first = done;
     for (int i = 0; done < nt; ++i, ++done) {
         cudaEvent_t e0 = timing ? g->tev[2 * i] : nullptr, e1 = timing ? g->tev[2 * i + 1] : nullptr;
-        aw_status st = enqueue_step(g, done - first, g->cur, g->steps + done, e0, e1, launches);
+        aw_status st = enqueue_step(g, done - first, g->cur, e0, e1, launches);
         if (st) return st;
         g->cur = 1 - g->cur;
     }
@@ -744,8 +799,11 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     aw_status st = leave(g);
     if (st) return st;
     CK(cudaStreamSynchronize(g->s));
-    unsigned flag = 0;
-    CK(cudaMemcpy(&flag, g->d_flag, sizeof flag, cudaMemcpyDeviceToHost));
+    aw::DevCtl ctl;
+    CK(cudaMemcpy(&ctl, g->ctl, sizeof ctl, cudaMemcpyDeviceToHost));
+    const unsigned flag = ctl.flag;
+    g->stats.ms_exchange = (double)ctl.wait_ns * 1e-6;
+    g->stats.exchange_waits = (int64_t)ctl.nwait;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, g->ev_t0, g->ev_t1));
     g->stats.ms_total = ms;
@@ -889,12 +947,15 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
         if (origin && !std::isfinite(origin[d])) return fail(AW_EINVAL, "origin[%d] not finite", d);
     }
     int rank = 0, world = 1, device = -1;
+    unsigned dflags = 0;
     cudaStream_t ext = nullptr;
     if (dist) {
         rank = dist->rank;
         world = dist->world;
         device = dist->device;
         ext = (cudaStream_t)dist->stream;
+        dflags = dist->flags;
+        if (dflags & ~(unsigned)AW_DIST_WORKSPACE) return fail(AW_EINVAL, "unknown aw_dist flags 0x%x", dflags);
         if (world < 1 || rank < 0 || rank >= world) return fail(AW_EINVAL, "bad rank/world %d/%d", rank, world);
     }
     int ndev = 0;
@@ -966,16 +1027,19 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
         if (bad(cudaEventCreate(&g->ev_t0), "event") || bad(cudaEventCreate(&g->ev_t1), "event")) break;
         g->ubytes = (size_t)(nz + 2 * R) * G.plane * sizeof(float);
         g->mbytes = (size_t)nz * G.plane * sizeof(float);
-        if (bad(cudaMalloc((void**)&g->ubuf[0], g->ubytes), "cudaMalloc u0")) break;
-        if (bad(cudaMalloc((void**)&g->ubuf[1], g->ubytes), "cudaMalloc u1")) break;
-        if (bad(cudaMalloc((void**)&g->m, g->mbytes), "cudaMalloc m")) break;
-        if (bad(cudaMalloc((void**)&g->b, g->mbytes), "cudaMalloc b")) break;
-        if (bad(cudaMalloc((void**)&g->d_base, sizeof(int64_t)), "cudaMalloc base")) break;
-        if (bad(cudaMalloc((void**)&g->d_flag, sizeof(unsigned)), "cudaMalloc flag")) break;
-        if (bad(cudaMalloc((void**)&g->d_team_flags, 2 * sizeof(unsigned long long)), "cudaMalloc flags")) break;
-        if (bad(cudaMemsetAsync(g->ubuf[0], 0, g->ubytes, g->s), "memset")) break;
-        if (bad(cudaMemsetAsync(g->ubuf[1], 0, g->ubytes, g->s), "memset")) break;
-        if (bad(cudaMemsetAsync(g->d_team_flags, 0, 2 * sizeof(unsigned long long), g->s), "memset")) break;
+        g->dense_bytes = 2 * align_up(g->ubytes, kDenseAlign) + 4 * align_up(g->mbytes, kDenseAlign);
+        if (bad(lmalloc(g, (void**)&g->ctl, sizeof(aw::DevCtl)), "cudaMalloc control block")) break;
+        g->d_base = &g->ctl->base;
+        g->d_flag = &g->ctl->flag;
+        g->d_team_flags = g->ctl->team_flags;
+        if (bad(cudaMemsetAsync(g->ctl, 0, sizeof(aw::DevCtl), g->s), "memset")) break;
+        if (!(dflags & AW_DIST_WORKSPACE)) {
+            if (bad(lmalloc(g, (void**)&g->dense_lib, g->dense_bytes), "cudaMalloc of the grid arrays")) break;
+            place_dense(g, g->dense_lib);
+            if (bad(cudaMemsetAsync(g->dense, 0, g->dense_bytes, g->s), "memset")) break;
+        }
+        if (bad(cudaMemcpyAsync(&g->ctl->epoch, &g->epoch, sizeof g->epoch, cudaMemcpyHostToDevice, g->s), "epoch"))
+            break;
         if (bad(cudaStreamSynchronize(g->s), "sync")) break;
     } while (0);
     if (st != AW_OK) {
@@ -996,22 +1060,20 @@ void aw_grid_destroy(aw_grid* g) {
     for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
     free_sources(g);
     free_receivers(g);
-    dfree(g->src_arena);
-    dfree(g->rec_arena);
-    dfree(g->adj_arena);
-    dfree(g->fwi_arena);
-    dfree(g->fwi_pool);
-    dfree(g->d_Gacc);
-    dfree(g->ubuf[0]);
-    dfree(g->ubuf[1]);
-    dfree(g->ubuf_spare);
-    dfree(g->m);
-    dfree(g->eta);
-    dfree(g->b);
-    dfree(g->a);
-    dfree(g->d_base);
-    dfree(g->d_flag);
-    dfree(g->d_team_flags);
+    dfree(g, g->src_arena);
+    dfree(g, g->rec_arena);
+    dfree(g, g->adj_arena);
+    dfree(g, g->fwi_arena);
+    dfree(g, g->fwi_pool);
+    dfree(g, g->d_Gacc);
+    // the third temporal-blocking buffer is the library's even when the rotation moved it into ubuf[]
+    for (float* p : {g->ubuf[0], g->ubuf[1], g->ubuf_spare})
+        if (p && g->lib_allocs.count((void*)p)) {
+            cudaFree(p);
+            g->lib_allocs.erase((void*)p);
+        }
+    dfree(g, g->dense_lib);
+    dfree(g, g->ctl);
     for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
     if (g->ev_sync) cudaEventDestroy(g->ev_sync);
     if (g->ev_t0) cudaEventDestroy(g->ev_t0);
@@ -1019,6 +1081,105 @@ void aw_grid_destroy(aw_grid* g) {
     if (g->s) cudaStreamDestroy(g->s);
     cudaGetLastError();
     delete g;
+}
+
+size_t aw_workspace_bytes(const aw_grid* g) {
+    if (!g) return 0;
+    return g->dense_bytes + align_up(g->src_need, 256) + align_up(g->rec_need, 256);
+}
+
+aw_status aw_bind_workspace(aw_grid* g, void* dev_ptr, size_t bytes) {
+    CHECK_STATE(g);
+    if (!dev_ptr) return fail(AW_EINVAL, "workspace pointer is NULL");
+    if ((uintptr_t)dev_ptr % 256) return fail(AW_EINVAL, "workspace must be 256-B aligned");
+    if (bytes < g->dense_bytes)
+        return fail(AW_EINVAL, "workspace of %zu B < the %zu B of the grid arrays", bytes, g->dense_bytes);
+    if (team_mode(g) && g->team_connected) return fail(AW_ESTATE, "bind the workspace before the team connects");
+    if (g->ws) return fail(AW_ESTATE, "a workspace is already bound to this handle");
+    {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, dev_ptr) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(AW_EINVAL, "workspace is not CUDA memory");
+        }
+        if (at.type != cudaMemoryTypeDevice || at.device != g->device)
+            return fail(AW_EINVAL, "workspace must be device memory on device %d", g->device);
+    }
+    char* nb = (char*)dev_ptr;
+    aw_status st = enter(g);
+    if (st) return st;
+    // 1. the dense block: copy the current contents (zeros when nothing was allocated yet)
+    char* old = g->dense;
+    if (old) CK(cudaMemcpyAsync(nb, old, g->dense_bytes, cudaMemcpyDeviceToDevice, g->s));
+    else CK(cudaMemsetAsync(nb, 0, g->dense_bytes, g->s));
+    // 2. the sparse arenas: source slot, then the receiver slot takes the rest of the workspace
+    const size_t tail0 = g->dense_bytes, tail = bytes - g->dense_bytes;
+    const size_t src_slot = std::min(tail, align_up(g->src_need, 256));
+    size_t slot_off[2] = {tail0, tail0 + src_slot};
+    size_t slot_cap[2] = {src_slot, tail - src_slot};
+    struct Move {
+        char** arena;
+        size_t* cap;
+        size_t need;
+    } mv[2] = {{&g->src_arena, &g->src_cap, g->src_need}, {&g->rec_arena, &g->rec_cap, g->rec_need}};
+    char* moved_from[2] = {nullptr, nullptr};
+    for (int k = 0; k < 2; ++k) {
+        if (*mv[k].arena && mv[k].need > 0 && mv[k].need <= slot_cap[k]) {
+            CK(cudaMemcpyAsync(nb + slot_off[k], *mv[k].arena, mv[k].need, cudaMemcpyDeviceToDevice, g->s));
+            moved_from[k] = *mv[k].arena;
+        }
+    }
+    CK(cudaStreamSynchronize(g->s));
+    // 3. repoint (everything below is host bookkeeping, nothing can fail)
+    auto rebase = [](auto*& p, char* from, size_t n, char* to) {
+        using T = std::remove_reference_t<decltype(*p)>;
+        if (p && (char*)p >= from && (char*)p < from + n) p = (T*)(to + ((char*)p - from));
+    };
+    if (old) {
+        for (float** p : {&g->ubuf[0], &g->ubuf[1], &g->ubuf_spare, &g->m, &g->eta, &g->b, &g->a})
+            rebase(*p, old, g->dense_bytes, nb);
+        g->dense = nb;
+    } else {
+        place_dense(g, nb);
+    }
+    for (int k = 0; k < 2; ++k) {
+        char* from = moved_from[k];
+        if (!from) continue;
+        char* to = nb + slot_off[k];
+        if (k == 0) {
+            rebase(g->d_wavelet, from, mv[k].need, to);
+            rebase(g->d_inj_off, from, mv[k].need, to);
+            rebase(g->d_inj_plane, from, mv[k].need, to);
+            rebase(g->d_inj_ptr, from, mv[k].need, to);
+            rebase(g->d_inj_src, from, mv[k].need, to);
+            rebase(g->d_inj_moff, from, mv[k].need, to);
+            rebase(g->d_inj_w64, from, mv[k].need, to);
+            rebase(g->d_inj_s, from, mv[k].need, to);
+        } else {
+            rebase(g->d_rec_id, from, mv[k].need, to);
+            rebase(g->d_rec_off, from, mv[k].need, to);
+            rebase(g->d_rec_w, from, mv[k].need, to);
+            rebase(g->d_traces, from, mv[k].need, to);
+        }
+    }
+    // free what now lives in the workspace: the library's dense block and the moved arenas
+    for (int k = 0; k < 2; ++k)
+        if (moved_from[k]) {
+            dfree(g, moved_from[k]);
+            *mv[k].arena = nb + slot_off[k];
+            *mv[k].cap = slot_cap[k];
+        }
+    dfree(g, g->dense_lib);
+    g->ws = nb;
+    g->ws_bytes = bytes;
+    for (int k = 0; k < 2; ++k) {
+        g->ws_slot_off[k] = slot_off[k];
+        g->ws_slot_cap[k] = slot_cap[k];
+    }
+    // every launch parameter, tensor map and captured graph that named the old addresses is rebuilt
+    g->coeffs_valid = false;
+    free_graphs(g);
+    return leave(g);
 }
 
 aw_status aw_local_extent(const aw_grid* g, int64_t* z0, int64_t* nz) {
@@ -1032,38 +1193,39 @@ int64_t aw_steps_done(const aw_grid* g) { return g ? g->steps : -1; }
 
 aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     if (!m) return fail(AW_EINVAL, "m is NULL");
     if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
     aw_status st = enter(g);
     if (st) return st;
     const int64_t nx = g->geom.nx, rows = (int64_t)g->geom.nz * g->geom.ny;
     const int64_t src_off = layout == AW_GLOBAL ? g->z0 * g->geom.ny * nx : 0;
-    if (damp && !g->eta) {
-        CK(cudaMalloc((void**)&g->eta, g->mbytes));
-        CK(cudaMalloc((void**)&g->a, g->mbytes));
-    }
-    // padding columns: m = 1, eta = 0 (never read as domain points)
-    CK(cudaMemsetAsync(g->m, 0, g->mbytes, g->s));
-    if ((st = copy_in(g, g->m, g->geom.pitch, m + src_off, nx, rows))) return st;
+    // Stage the new model in b (m) and a (eta): those hold dt-dependent coefficients that the next
+    // run recomputes anyway.  Validate the staged copy; only a valid model is swapped in, so an
+    // invalid one leaves the previous model in force (strong guarantee, include/aw.h).
+    float* new_m = g->b;
+    float* new_eta = g->a;
+    g->coeffs_valid = false;  // b and a are overwritten from here on
+    // padding columns (x >= nx): 0, never read as domain points
+    CK(cudaMemsetAsync(new_m, 0, g->mbytes, g->s));
+    if ((st = copy_in(g, new_m, g->geom.pitch, m + src_off, nx, rows))) return st;
     if (damp) {
-        CK(cudaMemsetAsync(g->eta, 0, g->mbytes, g->s));
-        if ((st = copy_in(g, g->eta, g->geom.pitch, damp + src_off, nx, rows))) return st;
+        CK(cudaMemsetAsync(new_eta, 0, g->mbytes, g->s));
+        if ((st = copy_in(g, new_eta, g->geom.pitch, damp + src_off, nx, rows))) return st;
     }
     CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
-    CK(aw::launch_validate_model(g->m, damp ? g->eta : nullptr, g->geom, g->d_flag, g->s));
+    CK(aw::launch_validate_model(new_m, damp ? new_eta : nullptr, g->geom, g->d_flag, g->s));
     g->launch_count += 1;
     unsigned flag = 0;
     CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof flag, cudaMemcpyDeviceToHost, g->s));
     CK(cudaStreamSynchronize(g->s));
     if ((st = leave(g))) return st;
-    if (flag) {
-        g->have_model = false;
-        g->coeffs_valid = false;
-        return fail(AW_EINVAL, "model invalid: m must be finite and > 0, damp finite and >= 0");
-    }
+    if (flag) return fail(AW_EINVAL, "model invalid: m must be finite and > 0, damp finite and >= 0 "
+                                     "(the previous model stays in force)");
+    std::swap(g->m, g->b);
+    if (damp) std::swap(g->eta, g->a);
     g->have_model = true;
     g->have_damp = damp != nullptr;
-    g->coeffs_valid = false;
     return AW_OK;
 }
 
@@ -1103,7 +1265,8 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
     const size_t small = pk.off;
     const size_t o_s = pk.reserve((size_t)g->nent * sizeof(float));
     const size_t o_wav = pk.reserve((size_t)nt_max * ns * sizeof(float));
-    if ((st = ensure_arena(g, &g->src_arena, &g->src_cap, pk.off))) return st;
+    if ((st = ensure_arena(g, &g->src_arena, &g->src_cap, pk.off, 0))) return st;
+    g->src_need = pk.off;
     char* A = g->src_arena;
     g->d_inj_off = (int64_t*)(A + o_off);
     g->d_inj_plane = (int*)(A + o_plane);
@@ -1166,7 +1329,8 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
     const size_t o_id = pk.add(ids), o_off = pk.add(offs), o_w = pk.add(ws);
     const size_t small = pk.off;
     const size_t o_tr = pk.reserve((size_t)nt_max * nr * sizeof(float));
-    if ((st = ensure_arena(g, &g->rec_arena, &g->rec_cap, pk.off))) return st;
+    if ((st = ensure_arena(g, &g->rec_arena, &g->rec_cap, pk.off, 1))) return st;
+    g->rec_need = pk.off;
     char* A = g->rec_arena;
     g->d_rec_id = (int*)(A + o_id);
     g->d_rec_off = (int64_t*)(A + o_off);
@@ -1180,6 +1344,7 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
 
 aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, int layout) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
     aw_status st = enter(g);
     if (st) return st;
@@ -1212,6 +1377,7 @@ aw_status aw_set_wavefield(aw_grid* g, const float* u_cur, const float* u_prev, 
         // already filled, so tell the neighbours they may proceed (their step stores into my
         // buffers only after this).  LOCAL: the exchange happens at the next aw_run (prologue).
         g->epoch += 1;
+        CK(cudaMemcpyAsync(&g->ctl->epoch, &g->epoch, sizeof g->epoch, cudaMemcpyHostToDevice, g->s));
         if (layout == AW_GLOBAL) {
             CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, g->steps), g->s));
             g->launch_count += 1;
@@ -1236,6 +1402,7 @@ aw_status aw_run(aw_grid* g, int nt, double dt) {
 aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, float* grad, int layout,
                           float* residual, double* objective) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     if (team_mode(g)) return fail(AW_EUNSUPPORTED, "aw_fwi_gradient runs on a single slab (world = 1)");
     if (nt < 1) return fail(AW_EINVAL, "nt must be >= 1 (got %d)", nt);
     if (!d_obs || !grad) return fail(AW_EINVAL, "d_obs/grad is NULL");
@@ -1286,11 +1453,10 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
         if (need > have) {
             if (g->fwi_pool) {
                 CK(cudaStreamSynchronize(g->s));
-                cudaFree(g->fwi_pool);
-                g->fwi_pool = nullptr;
+                dfree(g, g->fwi_pool);
                 g->fwi_pool_nbuf = 0;
             }
-            cudaError_t e = cudaMalloc((void**)&g->fwi_pool, (size_t)need * g->ubytes);
+            cudaError_t e = lmalloc(g, (void**)&g->fwi_pool, (size_t)need * g->ubytes);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 return fail(AW_ENOMEM, "FWI history pool of %lld buffers: %s", (long long)need, cudaGetErrorString(e));
@@ -1390,7 +1556,7 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     ++launches;
     const float* g_out = d_G;
     if (g->opt_accum) {  // NEXT-4: sum of the gradients of the calls since AW_OPT_FWI_ACCUMULATE was set
-        if (!g->d_Gacc) CK(cudaMalloc((void**)&g->d_Gacc, g->mbytes));
+        if (!g->d_Gacc) CK(lmalloc(g, (void**)&g->d_Gacc, g->mbytes));
         if (g->acc_valid) {
             CK(aw::launch_fwi_accumulate(g->geom, g->d_Gacc, d_G, g->s));
             ++launches;
@@ -1435,6 +1601,7 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
 
 aw_status aw_reset(aw_grid* g) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     aw_status st = enter(g);
     if (st) return st;
     CK(cudaMemsetAsync(g->ubuf[0], 0, g->ubytes, g->s));
@@ -1448,6 +1615,7 @@ aw_status aw_reset(aw_grid* g) {
     if (team_mode(g)) {
         // after my memsets: neighbours may start storing level-1 halos into my buffers
         g->epoch += 1;
+        CK(cudaMemcpyAsync(&g->ctl->epoch, &g->epoch, sizeof g->epoch, cudaMemcpyHostToDevice, g->s));
         CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, 0), g->s));
         g->launch_count += 1;
     }
@@ -1457,6 +1625,7 @@ aw_status aw_reset(aw_grid* g) {
 
 aw_status aw_read_wavefield(aw_grid* g, int which, float* out, int layout) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     if (!out) return fail(AW_EINVAL, "out is NULL");
     if (which != 0 && which != 1) return fail(AW_EINVAL, "which must be 0 or 1");
     if (layout != AW_GLOBAL && layout != AW_LOCAL) return fail(AW_EINVAL, "bad layout %d", layout);
@@ -1512,6 +1681,10 @@ aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out) {
     if (!g || !out) return fail(AW_EINVAL, "null argument");
     *out = g->stats;
     out->launches_total = g->launch_count;
+    int64_t lib = 0;
+    for (const auto& kv : g->lib_allocs) lib += (int64_t)kv.second;
+    out->lib_device_bytes = lib + (int64_t)aw::stream_plan_bytes(g->plan);
+    out->workspace_bytes = (int64_t)g->ws_bytes;
     return AW_OK;
 }
 
@@ -1564,12 +1737,55 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
 // ---------------------------------------------------------------------------
 // Teams
 // ---------------------------------------------------------------------------
+// A peer address = (IPC handle of the allocation that contains it, offset into it): the wavefield
+// levels share one allocation (the dense block or the caller's workspace) and the flag words sit
+// inside the control block, so none of them is an allocation base.
+struct aw_ipc_ptr {
+    cudaIpcMemHandle_t h;
+    int64_t off;
+};
 struct aw_team_record {
-    cudaIpcMemHandle_t u[2];
-    cudaIpcMemHandle_t flags;
+    aw_ipc_ptr u[2];
+    aw_ipc_ptr flags;
     int64_t nz, R, plane, ny, nx;
     int32_t rank, world;
 };
+
+namespace {
+typedef int (*PFN_memGetAddressRange)(unsigned long long*, size_t*, unsigned long long);  // cuMemGetAddressRange_v2
+aw_status ipc_export(aw_grid* g, const void* p, aw_ipc_ptr* out) {
+    static PFN_memGetAddressRange fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return fail(AW_ECUDA, "cuMemGetAddressRange is unavailable");
+        fn = (PFN_memGetAddressRange)f;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (unsigned long long)(uintptr_t)p) != 0) return fail(AW_ECUDA, "cuMemGetAddressRange failed");
+    CK(cudaIpcGetMemHandle(&out->h, (void*)(uintptr_t)base));
+    out->off = (int64_t)((uintptr_t)p - (uintptr_t)base);
+    return AW_OK;
+}
+// Open a peer address; every distinct handle is opened once per handle (re-opening an open
+// handle in the same process is an error) and kept until aw_grid_destroy.
+aw_status ipc_open(aw_grid* g, const aw_ipc_ptr& ip, void** out) {
+    for (const auto& o : g->ipc_opened_h)
+        if (std::memcmp(&o.first, &ip.h, sizeof ip.h) == 0) {
+            *out = (char*)o.second + ip.off;
+            return AW_OK;
+        }
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, ip.h, cudaIpcMemLazyEnablePeerAccess));
+    g->ipc_opened.push_back(base);
+    g->ipc_opened_h.push_back({ip.h, base});
+    *out = (char*)base + ip.off;
+    return AW_OK;
+}
+}  // namespace
 
 size_t aw_team_export_size(void) { return sizeof(aw_team_record); }
 
@@ -1586,13 +1802,15 @@ aw_status aw_slab_partition(int64_t n0, int world, int rank, int R, int64_t* z0,
 
 aw_status aw_team_export(aw_grid* g, void* out) {
     CHECK_STATE(g);
+    NEED_DENSE(g);
     if (!out) return fail(AW_EINVAL, "out is NULL");
     aw_team_record rec;
     std::memset(&rec, 0, sizeof rec);
     CK(cudaSetDevice(g->device));
-    CK(cudaIpcGetMemHandle(&rec.u[0], g->ubuf[0]));
-    CK(cudaIpcGetMemHandle(&rec.u[1], g->ubuf[1]));
-    CK(cudaIpcGetMemHandle(&rec.flags, g->d_team_flags));
+    aw_status st;
+    if ((st = ipc_export(g, g->ubuf[0], &rec.u[0])) || (st = ipc_export(g, g->ubuf[1], &rec.u[1])) ||
+        (st = ipc_export(g, g->d_team_flags, &rec.flags)))
+        return st;
     rec.nz = g->geom.nz;
     rec.R = g->R;
     rec.plane = g->geom.plane;
@@ -1638,12 +1856,10 @@ aw_status aw_team_connect(aw_grid* g, const void* all_records) {
     for (int k = 0; k < 2; ++k) {
         int r = nb[k];
         if (r < 0 || r >= g->world) continue;
-        for (int b = 0; b < 2; ++b) {
-            CK(cudaIpcOpenMemHandle(&p[k][b], recs[r].u[b], cudaIpcMemLazyEnablePeerAccess));
-            g->ipc_opened.push_back(p[k][b]);
-        }
-        CK(cudaIpcOpenMemHandle(&f[k], recs[r].flags, cudaIpcMemLazyEnablePeerAccess));
-        g->ipc_opened.push_back(f[k]);
+        aw_status st;
+        if ((st = ipc_open(g, recs[r].u[0], &p[k][0])) || (st = ipc_open(g, recs[r].u[1], &p[k][1])) ||
+            (st = ipc_open(g, recs[r].flags, &f[k])))
+            return st;
     }
     int64_t nz_lo = g->rank > 0 ? recs[g->rank - 1].nz : 0;
     link_neighbours(g, (float*)p[0][0], (float*)p[0][1], (unsigned long long*)f[0], nz_lo, (float*)p[1][0],
@@ -1711,7 +1927,7 @@ aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt) {
             }
             cudaEvent_t e0 = g->opt_timing ? g->tev[2 * i] : nullptr, e1 = g->opt_timing ? g->tev[2 * i + 1] : nullptr;
             CK(cudaSetDevice(g->device));
-            aw_status st = enqueue_step(g, i, g->cur, g->steps + i, e0, e1, &launches[r]);
+            aw_status st = enqueue_step(g, i, g->cur, e0, e1, &launches[r]);
             if (st) return st;
             g->cur = 1 - g->cur;
         }

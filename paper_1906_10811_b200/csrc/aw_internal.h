@@ -49,6 +49,20 @@ struct Halo {
     int64_t hi_off; // element offset of rank+1's plane -R relative to its base (= 0)
 };
 
+// Device control words of one handle (one small allocation).  base = global index of the step a
+// launch calls step 0 (kernels take a step offset i, so CUDA graphs replay unchanged); epoch =
+// team epoch (bumped by reset / set_wavefield); team_flags are written by the neighbours (exported
+// through cudaIpc) with levels encoded (epoch << 32) + level + 1.
+struct DevCtl {
+    int64_t base;
+    unsigned long long epoch;
+    unsigned long long wait_ns;  // team: device time spent waiting for halo planes (last run)
+    unsigned long long nwait;    // team: waits that blocked (last run)
+    unsigned flag;               // non-finite result / invalid model
+    unsigned pad_[7];
+    unsigned long long team_flags[2];  // [0]: from rank-1, [1]: from rank+1
+};
+
 // Sparse (receivers + injection CSR) device view
 struct Sparse {
     // receivers owned by this rank
@@ -88,10 +102,9 @@ cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucu
 cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s);
 cudaError_t launch_check_finite(const Geom& g, const float* u, const float* traces, int64_t t0,
                                 int64_t t1, int nr, unsigned* flag, cudaStream_t s);
-cudaError_t launch_team_wait(const volatile unsigned long long* flags, unsigned long long want_lo,
-                             unsigned long long want_hi, cudaStream_t s);
+cudaError_t launch_team_wait(DevCtl* ctl, bool has_lo, bool has_hi, int i, cudaStream_t s);
 cudaError_t launch_team_signal(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
-                               unsigned long long add, const int64_t* d_base, int i, cudaStream_t s);
+                               const DevCtl* ctl, int i, cudaStream_t s);
 cudaError_t launch_team_raise(unsigned long long* f0, unsigned long long* f1, unsigned long long v,
                               cudaStream_t s);
 
@@ -104,6 +117,7 @@ cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubu
                            cudaStream_t s);
 int stream_eta_tiles_pct(const StreamPlan* p);
 void stream_release(StreamPlan* p);
+size_t stream_plan_bytes(const StreamPlan* p);  // device bytes the plan holds (NULL -> 0)
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
                                   const float* ucur, float* unext, const float* b, const float* a,
                                   const Halo& halo, int parity_next, const Sparse& sp, const int64_t* d_base,

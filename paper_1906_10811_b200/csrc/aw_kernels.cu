@@ -266,38 +266,52 @@ cudaError_t launch_check_finite(const Geom& g, const float* u, const float* trac
 // it also certifies that the neighbour finished reading the halo buffer that
 // the next step overwrites (no WAR hazard with two physical levels).
 // ---------------------------------------------------------------------------
-__global__ void team_wait_kernel(const volatile unsigned long long* flags, unsigned long long want_lo,
-                                 unsigned long long want_hi) {
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Levels are encoded (epoch << 32) + level + 1 with the epoch and the step base read from the
+// device control block, so the kernels are parameter-free per step and can be graph-captured.
+__global__ void team_wait_kernel(DevCtl* ctl, int has_lo, int has_hi, int i) {
     if (threadIdx.x != 0) return;
-    // flags[0]: from rank-1, flags[1]: from rank+1
-    for (;;) {
+    const unsigned long long want = (ctl->epoch << 32) + (unsigned long long)(ctl->base + i + 1);
+    // team_flags[0]: from rank-1, [1]: from rank+1
+    const volatile unsigned long long* flags = ctl->team_flags;
+    unsigned long long t0 = 0;
+    for (int k = 0;; ++k) {
         unsigned long long f0, f1;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f0) : "l"(flags + 0) : "memory");
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f1) : "l"(flags + 1) : "memory");
-        if (f0 >= want_lo && f1 >= want_hi) break;
+        if ((!has_lo || f0 >= want) && (!has_hi || f1 >= want)) break;
+        if (k == 0) t0 = global_ns();
         __nanosleep(200);
+    }
+    if (t0) {  // exchange-time accounting (aw_run_stats.ms_exchange)
+        ctl->wait_ns += global_ns() - t0;
+        ctl->nwait += 1;
     }
 }
 
-cudaError_t launch_team_wait(const volatile unsigned long long* flags, unsigned long long want_lo,
-                             unsigned long long want_hi, cudaStream_t s) {
-    team_wait_kernel<<<1, 32, 0, s>>>(flags, want_lo, want_hi);
+cudaError_t launch_team_wait(DevCtl* ctl, bool has_lo, bool has_hi, int i, cudaStream_t s) {
+    team_wait_kernel<<<1, 32, 0, s>>>(ctl, has_lo, has_hi, i);
     return cudaGetLastError();
 }
 
 __global__ void team_signal_kernel(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
-                                   unsigned long long add, const int64_t* d_base, int i) {
+                                   const DevCtl* ctl, int i) {
     if (threadIdx.x != 0) return;
-    // enc(level) = (epoch << 32) + level + 1; this step produced level *d_base + i + 1
-    unsigned long long v = add + (unsigned long long)(*d_base + i + 2);
+    // this step produced level base + i + 1
+    unsigned long long v = (ctl->epoch << 32) + (unsigned long long)(ctl->base + i + 2);
     __threadfence_system();  // halo stores of this step (stencil + injection) before the flag
     if (peer_lo_flag) atomicMax_system(peer_lo_flag, v);
     if (peer_hi_flag) atomicMax_system(peer_hi_flag, v);
 }
 
 cudaError_t launch_team_signal(unsigned long long* peer_lo_flag, unsigned long long* peer_hi_flag,
-                               unsigned long long add, const int64_t* d_base, int i, cudaStream_t s) {
-    team_signal_kernel<<<1, 32, 0, s>>>(peer_lo_flag, peer_hi_flag, add, d_base, i);
+                               const DevCtl* ctl, int i, cudaStream_t s) {
+    team_signal_kernel<<<1, 32, 0, s>>>(peer_lo_flag, peer_hi_flag, ctl, i);
     return cudaGetLastError();
 }
 

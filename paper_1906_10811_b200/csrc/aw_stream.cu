@@ -123,6 +123,17 @@ int stream_eta_tiles_pct(const StreamPlan* p) {
     return p->nflags ? (int)(100.0 * (double)h / (double)p->nflags + 0.5) : 0;
 }
 
+size_t stream_plan_bytes(const StreamPlan* p) {
+    if (!p) return 0;
+    size_t n = p->flags ? (size_t)p->nflags + sizeof(unsigned long long) + 16 : 0;
+    for (int k = 0; k < 2; ++k) {
+        if (p->tpsc[k]) n += (size_t)p->nflags * sizeof(int2);
+        n += p->tpe_cap[k] * sizeof(int4);
+    }
+    if (p->tb_done) n += (size_t)p->tb_nzc * p->ntx * p->nty * sizeof(unsigned long long);
+    return n;
+}
+
 void stream_release(StreamPlan* p) {
     if (!p) return;
     if (p->flags) cudaFree(p->flags);
