@@ -54,7 +54,10 @@ def parse():
                     help="NEXT-1 temporal blocking: two time steps per launch (single slab, 3D)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle time steps in the cpu_baseline sample")
+    ap.add_argument("--cpu-steps", type=int, default=50,
+                    help="oracle time steps timed for cpu_baseline (SURVEY §8(d): >= 50, setup excluded)")
+    ap.add_argument("--ref-steps", type=int, default=3,
+                    help="oracle time steps per bench step of the --impl reference arm (bounded sample)")
     return ap.parse_args()
 
 
@@ -75,9 +78,12 @@ def load_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+    """nvidia-smi sampling of the clocks (the recipe's clocks line).  The sampler starts BEFORE the
+    warm-up steps and the bench waits for its first sample, so its start-up (NVML initialisation,
+    which can stall short GPU work) stays out of the timed region; samples are then filtered to the
+    timed window by their timestamps (all samples if the window is shorter than the 200-ms period)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -86,7 +92,7 @@ class Clocks:
         self.proc = None
         self.path = None
 
-    def start(self):
+    def start(self, wait_s=5.0):
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
@@ -94,10 +100,21 @@ class Clocks:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.out,
                                          stderr=subprocess.DEVNULL)
+            t_end = time.time() + wait_s
+            while time.time() < t_end and os.path.getsize(self.path) == 0:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
 
-    def stop(self):
+    @staticmethod
+    def _epoch(stamp):
+        import datetime
+        try:
+            return datetime.datetime.strptime(stamp.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
+    def stop(self, window=None):
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -106,26 +123,29 @@ class Clocks:
         except Exception:
             self.proc.kill()
         self.out.close()
-        sm, smax, reasons = [], None, set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
+                if len(parts) < 10:
                     continue
                 try:
-                    sm.append(float(parts[1]))
-                    smax = float(parts[2])
+                    rows.append((self._epoch(parts[0]), float(parts[2]), float(parts[3]),
+                                 {n for n, v in zip(names, parts[6:10]) if v.lower().startswith("active")}))
                 except ValueError:
                     continue
-                for n, v in zip(names, parts[5:9]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
         os.unlink(self.path)
-        if not sm:
+        if not rows:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sel, where = rows, "warm-up + timed region"
+        if window:
+            inside = [r for r in rows if r[0] is not None and window[0] - 0.25 <= r[0] <= window[1] + 0.25]
+            if inside:
+                sel, where = inside, "timed region"
+        reasons = set().union(*[r[3] for r in sel])
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": sel[-1][2], "reasons": sorted(reasons),
+                "samples": len(sel), "sampled": where}
 
 
 # ---------------------------------------------------------------------------
@@ -177,16 +197,21 @@ def local_model(spec, z0, nz, device):
 # ---------------------------------------------------------------------------
 # the reference arm / cpu baseline: the oracle as it stands, on a bounded sample
 # ---------------------------------------------------------------------------
-def oracle_sample(spec, nsteps):
-    import oracle
+def oracle_inputs(spec):
     import workloads as W
     shape = spec["shape"]
     if "arrays" in spec:
-        m, damp = spec["arrays"].m, spec["arrays"].damp
-    else:
-        m = W.random_smooth_m(shape)
-        damp = W.damping_profile(shape, spec["nbl"])
-    wav = W.ricker(nsteps, spec["dt"], spec["f0"], ns=len(spec["src"]))
+        return spec["arrays"].m, spec["arrays"].damp
+    return W.random_smooth_m(shape), W.damping_profile(shape, spec["nbl"])
+
+
+def oracle_sample(spec, nsteps, inputs=None):
+    """Whole oracle_run call of nsteps steps (setup included): (Gpts/s, seconds, threads)."""
+    import oracle
+    import workloads as W
+    shape = spec["shape"]
+    m, damp = inputs if inputs is not None else oracle_inputs(spec)
+    wav = W.ricker(max(nsteps, 1), spec["dt"], spec["f0"], ns=len(spec["src"]))
     extent = [10.0 * (n - 1) for n in shape]
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
@@ -195,6 +220,40 @@ def oracle_sample(spec, nsteps):
     t = time.perf_counter() - t0
     pts = float(np.prod(shape)) * nsteps
     return pts / t / 1e9, t, threads
+
+
+def host_info():
+    """The CPU the oracle runs on (lscpu model/sockets, binding, numactl)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    info["OMP_PROC_BIND"] = os.environ.get("OMP_PROC_BIND")
+    info["OMP_PLACES"] = os.environ.get("OMP_PLACES")
+    import shutil
+    info["numactl"] = "numactl --interleave=all" if shutil.which("numactl") else "not installed (one NUMA node)"
+    return info
+
+
+def cpu_baseline(spec, nsteps):
+    """SURVEY §8(d) protocol: the oracle (fp32canon, all host cores, OMP_PROC_BIND=close) timed over
+    nsteps time steps with its setup excluded -- t(1 + nsteps) - t(1) -- as a per-step rate,
+    extrapolated to the workload's nt."""
+    inputs = oracle_inputs(spec)
+    _, t_one, threads = oracle_sample(spec, 1, inputs)
+    _, t_all, _ = oracle_sample(spec, 1 + nsteps, inputs)
+    t = max(t_all - t_one, 1e-9)
+    v = float(np.prod(spec["shape"])) * nsteps / t / 1e9
+    return {"value": round(v, 5), "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+            "sample": f"{spec['name']} grid {list(spec['shape'])}, so {spec['so']}: {nsteps} time steps timed as "
+                      f"t({1 + nsteps} steps) - t(1 step) = {t:.1f} s (setup excluded); per-step rate, "
+                      f"extrapolated to the {spec['nt']}-step workload",
+            "extrapolated": True, "setup_s": round(t_one, 2), "host": host_info()}
 
 
 def bench_config(spec, nt, world, pts_local, damped):
@@ -218,7 +277,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     spec = workload_spec(args.workload, 1 if world == 1 else world)
-    nsteps = args.cpu_steps
+    nsteps = args.ref_steps
     vals, secs = [], []
     for _ in range(max(0, min(args.warmup, 1))):
         oracle_sample(spec, 1)
@@ -239,7 +298,7 @@ def run_reference(args, rank, world):
                                    float(spec["shape"][0] // world) * float(np.prod(spec["shape"][1:])),
                                    spec["nbl"] > 0),
             "cpu_baseline": {"value": round(value, 4), "unit": "Gpts/s", "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": round(value, 4), "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -248,6 +307,9 @@ def run_reference(args, rank, world):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    # the oracle's OpenMP threads stay on their cores; read when libgomp initialises
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -283,13 +345,13 @@ def main():
     extent = [10.0 * (n - 1) for n in shape]
     stream = torch.cuda.current_stream()
 
-    g = aw.Grid(shape, extent, spec["so"], rank=rank, world=world, device=local, stream=stream)
+    # torch owns the device memory (north star; include/aw.h aw_bind_workspace): the grid is created
+    # without arrays, the sparse points are added once to size their arenas, then one uint8 tensor
+    # holds the wavefields, m, eta, b, a and both arenas
+    g = aw.Grid(shape, extent, spec["so"], rank=rank, world=world, device=local, stream=stream, workspace="defer")
     if args.kernel != "auto":
         g.set_option(aw.AW_OPT_KERNEL, {"v1": aw.AW_KERNEL_V1, "stream": aw.AW_KERNEL_STREAM}[args.kernel])
     g.set_option(aw.AW_OPT_TEMPORAL, args.temporal)
-    if world > 1:
-        from paper_1906_10811_b200 import team
-        team.connect(g)  # cudaIpc records all-gathered in rank order -> aw_team_connect
 
     import workloads as W
     m_dev, d_dev = local_model(spec, g.z0, g.nz, device)
@@ -297,6 +359,14 @@ def main():
     wav_dev = torch.from_numpy(wav).to(device)
     nr = len(spec["rec"])
     traces_dev = torch.zeros((nt, nr), dtype=torch.float32, device=device)
+    g.add_sources(spec["src"], wav_dev)
+    g.add_receivers(spec["rec"], nt)
+    workspace = g.bind_workspace()
+    if world > 1:
+        from paper_1906_10811_b200 import team
+        team.connect(g)  # cudaIpc records all-gathered in rank order -> aw_team_connect
+    # SURVEY §8(d) f_eta: fraction of the points where eta != 0 (the `a` stream is algorithmic there)
+    f_eta = float(torch.count_nonzero(d_dev).item()) / d_dev.numel() if d_dev is not None else 0.0
     torch.cuda.synchronize()
 
     def barrier():
@@ -309,6 +379,7 @@ def main():
         return float(t.item())
 
     verbose = bool(os.environ.get("AW_BENCH_VERBOSE"))
+    call_ms = {}  # AW_BENCH_VERBOSE: host wall time per ABI call, summed (printed at the end)
 
     def one_step(m, d, wv, traces):
         calls = (("barrier", barrier), ("reset", g.reset), ("set_model", lambda: g.set_model(m, d, aw.AW_LOCAL)),
@@ -321,36 +392,46 @@ def main():
             t0 = time.perf_counter()
             fn()
             dt_ms = 1e3 * (time.perf_counter() - t0)
-            if verbose and (dt_ms > 20 and name != "run"):
-                print(f"  slow call {name}: {dt_ms:.1f} ms", file=sys.stderr, flush=True)
+            if verbose:
+                call_ms[name] = call_ms.get(name, 0.0) + dt_ms
 
-    # the timed region runs the production path (per-launch timing off: CUDA graphs of several steps
-    # where the library uses them); the roofline pass below repeats the K steps with per-launch events
-    g.set_option(aw.AW_OPT_TIMING, 0)
+    # the timed region runs the production path (CUDA graphs of 16 steps).  With the 3D streaming kernel
+    # the library stamps every stencil launch with the device clock inside it (AW_OPT_TIMING = 2: first
+    # CTA start, last CTA end; graphs kept), so the roofline comes from the headline region itself;
+    # other kernels (v1, 2D) get a second pass with per-launch CUDA events
+    dev_ts = args.kernel != "v1" and len(shape) == 3 and not args.temporal
+    g.set_option(aw.AW_OPT_TIMING, 2 if dev_ts else 0)
+    clocks = Clocks(local)
+    if not os.environ.get("AW_BENCH_NO_CLOCKS"):
+        clocks.start()  # before the warm-up: its start-up stays out of the timed region
     for _ in range(args.warmup):
         one_step(m_dev, d_dev, wav_dev, traces_dev)
 
     # ---- timed region: K steps, inputs resident in HBM ----
-    clocks = Clocks(local)
     launches0 = g.stats()["launches_total"]
     torch.cuda.synchronize()
     barrier()
     gc.collect()
     gc.disable()  # no collector pauses inside the timed region
-    if not os.environ.get("AW_BENCH_NO_CLOCKS"):
-        clocks.start()
+    t_win0 = time.time()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    ms_stencil, n_stencil, ms_xchg = 0.0, 0, 0.0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         one_step(m_dev, d_dev, wav_dev, traces_dev)
+        st = g.stats()
+        if dev_ts:
+            ms_stencil += st["ms_stencil"]
+            n_stencil += st["n_stencil"]
+        ms_xchg += st["ms_exchange"]
         if verbose:
-            print(f"step: wall {1e3 * (time.perf_counter() - t0):.2f} ms, run {g.stats()['ms_total']:.2f} ms",
+            print(f"step: wall {1e3 * (time.perf_counter() - t0):.2f} ms, run {st['ms_total']:.2f} ms",
                   file=sys.stderr, flush=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop((t_win0, time.time()))
     gc.enable()
     ms = ev0.elapsed_time(ev1)
     launches = g.stats()["launches_total"] - launches0
@@ -359,23 +440,24 @@ def main():
     total_pts = float(np.prod(shape)) * nt * args.steps
     value = total_pts / (ms * 1e-3) / 1e9
 
-    # ---- roofline pass: the same K steps again with per-launch CUDA events on the library's stream ----
-    g.set_option(aw.AW_OPT_TIMING, 1)
-    one_step(m_dev, d_dev, wav_dev, traces_dev)  # creates the event pool
-    torch.cuda.synchronize()
-    barrier()
-    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    r0.record(stream)
-    ms_stencil, n_stencil = 0.0, 0
-    for _ in range(args.steps):
-        one_step(m_dev, d_dev, wav_dev, traces_dev)
-        st = g.stats()
-        ms_stencil += st["ms_stencil"]
-        n_stencil += st["n_stencil"]
-    r1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms_rpass = r0.elapsed_time(r1)
+    ms_rpass = ms
+    if not dev_ts:
+        # ---- roofline pass (v1 / 2D / temporal blocking): the K steps again with per-launch CUDA events ----
+        g.set_option(aw.AW_OPT_TIMING, 1)
+        one_step(m_dev, d_dev, wav_dev, traces_dev)  # creates the event pool
+        torch.cuda.synchronize()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.steps):
+            one_step(m_dev, d_dev, wav_dev, traces_dev)
+            st = g.stats()
+            ms_stencil += st["ms_stencil"]
+            n_stencil += st["n_stencil"]
+        r1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_rpass = r0.elapsed_time(r1)
 
     # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region ----
     e2e = None
@@ -428,19 +510,18 @@ def main():
                 "steps_per_launch": steps_per_launch, "peak_source": peak_src,
                 "stencil_ms_avg": round(avg_ms, 4),
                 "stencil_share_of_step": round(ms_stencil / ms_rpass, 4) if ms_rpass else None,
-                "measured_in": "a second pass of the same K bench steps with per-launch CUDA events on the "
-                               "library stream (the headline timed region runs without them)",
+                "measured_in": ("the headline timed region itself: the streaming kernel stamps each launch's first "
+                                "CTA start and last CTA end with %globaltimer (AW_OPT_TIMING=2, CUDA graphs kept)"
+                                if dev_ts else "a second pass of the same K bench steps with per-launch CUDA "
+                                "events on the library stream (the headline region runs without them)"),
                 # the strict one-step streaming floor (16 B per point update) at the achieved update rate
                 "vs_streaming_floor": round(B_STRICT * pts_local / (ms_stencil / max(1, n_stencil) * 1e-3) / 1e9
                                             / peak, 4) if ms_stencil > 0 else None}
 
-    # ---- cpu baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
+    # ---- cpu baseline: the oracle, >= 50 steps with setup excluded (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, t, threads = oracle_sample(spec, args.cpu_steps)
-        cpu = {"value": round(v, 5), "unit": "Gpts/s", "cores": threads, "kind": "oracle",
-               "sample": f"{spec['name']} grid {list(shape)}, so {spec['so']}, {args.cpu_steps} time steps "
-                         f"(whole oracle_run call, {t:.1f} s)"}
+        cpu = cpu_baseline(spec, args.cpu_steps)
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world, "steps": args.steps,
@@ -448,12 +529,19 @@ def main():
                 "scaling": spec.get("scaling", "weak"), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": bench_config(spec, nt, world, pts_local, d_dev is not None),
                 "hbm_pct_strict": round(100 * value * B_STRICT / world / peak, 2),
-                # SURVEY §8(d) B_alg = 16 + 4 f_eta: the `a` stream is read in the tile-planes that hold damping
-                "hbm_pct_alg": round(100 * value * (B_STRICT + 4 * st["eta_tiles"] / 100.0) / world / peak, 2),
+                # SURVEY §8(d) B_alg = 16 + 4 f_eta, f_eta = fraction of the points with eta != 0
+                "hbm_pct_alg": round(100 * value * (B_STRICT + 4 * f_eta) / world / peak, 2),
+                "f_eta": round(f_eta, 4),
+                # the kernel streams `a` per tile-plane: tile-planes holding any damping (its own over-read)
                 "eta_tile_planes_pct": st["eta_tiles"],
+                "workspace_bytes": int(st["workspace_bytes"]), "lib_device_bytes": int(st["lib_device_bytes"]),
+                "ms_exchange_per_step": round(ms_xchg / args.steps, 3) if world > 1 else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk}
         print(json.dumps(line), flush=True)
+    if verbose:
+        print("host ms per call (all passes): " + json.dumps({k: round(v, 2) for k, v in call_ms.items()}),
+              file=sys.stderr, flush=True)
     g.close()
     if world > 1:
         dist.destroy_process_group()

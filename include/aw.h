@@ -72,7 +72,10 @@ enum { AW_KERNEL_AUTO = 0 /* STREAM in 3D, TILE2D in 2D */, AW_KERNEL_V1 = 1 /* 
 /* options */
 enum {
     AW_OPT_KERNEL = 1,      /* value: AW_KERNEL_* */
-    AW_OPT_TIMING = 2,      /* value 1: time every stencil launch with CUDA events (no graphs) */
+    AW_OPT_TIMING = 2,      /* value 1: time every stencil launch with CUDA events (direct launches, no graphs);
+                               value 2: the 3D streaming kernel stamps its first-CTA start and last-CTA end
+                               per launch with the device clock (%globaltimer), CUDA graphs kept -- the
+                               production path; aw_run_stats.ms_stencil / n_stencil report them */
     AW_OPT_GRAPH_STEPS = 3, /* value G >= 0: steps per captured CUDA graph (0 = no graphs) */
     AW_OPT_CHECK_FINITE = 4, /* value 0/1 (default 1): aw_run checks traces + final field */
     AW_OPT_CHECKPOINT_STEPS = 5, /* value K >= 0: aw_fwi_gradient segment length (0 = auto, see there) */

@@ -97,6 +97,8 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 for _name, (_res, _args) in _SIGS.items():
+    if os.environ.get("AW_LIBRARY") and not hasattr(_lib, _name):
+        continue  # an older build under A/B measurement (tools/ab_stream.py) may lack newer calls
     _fn = getattr(_lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args

@@ -174,7 +174,14 @@ struct aw_grid {
     int eta_tiles_pct = 100;
     int kernel_used = AW_KERNEL_V1;
     // graphs: key = (G << 1) | parity
-    std::map<int64_t, cudaGraphExec_t> graphs;
+    // captured graphs per (G, parity): a few entries, each with the signature of every launch parameter
+    // it captured (buffers, tensor maps, sparse tables, ...), so a setup call that changes nothing the
+    // graph uses (e.g. the same sources re-added, a new model in the same arrays) keeps the graph
+    struct GraphEntry {
+        std::string sig;
+        cudaGraphExec_t exec;
+    };
+    std::map<int64_t, std::vector<GraphEntry>> graphs;
     // timing events pool
     std::vector<cudaEvent_t> tev;
     // team
@@ -224,6 +231,10 @@ struct aw_grid {
     float* ubuf_spare = nullptr;
     bool tb_ready = false;
     int n_timed = 0;                       // timed stencil launches of the last run (AW_OPT_TIMING)
+    unsigned long long* ts0 = nullptr;     // AW_OPT_TIMING = 2: per-launch first-CTA start (device ns)
+    unsigned long long* ts1 = nullptr;     //                    per-launch last-CTA end
+    int ts_cap = 0;
+    bool ts_on = false;                    // the last run recorded device timestamps
     bool wave_invalid = false;             // after aw_fwi_gradient until aw_reset / aw_set_wavefield
 };
 
@@ -245,7 +256,8 @@ namespace {
     } while (0)
 
 void free_graphs(aw_grid* g) {
-    for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : g->graphs)
+        for (auto& e : kv.second) cudaGraphExecDestroy(e.exec);
     g->graphs.clear();
 }
 
@@ -513,7 +525,8 @@ aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes, int 
 }
 
 aw::Sparse sparse_view(const aw_grid* g) {
-    aw::Sparse sp{};
+    aw::Sparse sp;
+    std::memset(&sp, 0, sizeof sp);  // padding too: the bytes are part of graph signatures
     sp.nrl = g->nrl;
     sp.nr = g->nr;
     sp.rec_id = g->d_rec_id;
@@ -583,7 +596,6 @@ aw_status prepare(aw_grid* g, double dt) {
         if (!g->t2) CK(aw::tile2d_prepare(g->geom, &g->t2));
         g->kernel_used = AW_KERNEL_TILE2D;
     }
-    free_graphs(g);
     g->dt = dt;
     g->dt_set = true;
     g->coeffs_valid = true;
@@ -630,13 +642,39 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, cudaEvent_t e0, cudaEvent_t e
     return AW_OK;
 }
 
+// Every value a captured step launch takes from the handle (see enqueue_step).
+std::string graph_signature(const aw_grid* g) {
+    std::string sig;
+    auto put = [&](const void* p, size_t n) { sig.append((const char*)p, n); };
+    put(&g->kernel_used, sizeof g->kernel_used);
+    put(g->ubuf, sizeof g->ubuf);
+    put(&g->b, sizeof g->b);
+    const float* a = g->have_damp ? g->a : nullptr;
+    put(&a, sizeof a);
+    put(&g->coefs, sizeof g->coefs);
+    put(&g->geom, sizeof g->geom);
+    const aw::Sparse sp = sparse_view(g);
+    put(&sp, sizeof sp);
+    put(&g->halo, sizeof g->halo);
+    put(&g->peer_flag_lo, sizeof g->peer_flag_lo);
+    put(&g->peer_flag_hi, sizeof g->peer_flag_hi);
+    put(&g->ctl, sizeof g->ctl);
+    put(&g->t2, sizeof g->t2);
+    put(&g->plan, sizeof g->plan);
+    aw::stream_plan_signature(g->plan, &sig);
+    return sig;
+}
+
 aw_status get_graph(aw_grid* g, int G, int cur, cudaGraphExec_t* out) {
-    int64_t key = ((int64_t)G << 1) | cur;
-    auto it = g->graphs.find(key);
-    if (it != g->graphs.end()) {
-        *out = it->second;
-        return AW_OK;
-    }
+    const int64_t key = ((int64_t)G << 1) | cur;
+    const std::string sig = graph_signature(g);
+    std::vector<aw_grid::GraphEntry>& ents = g->graphs[key];
+    for (size_t k = 0; k < ents.size(); ++k)
+        if (ents[k].sig == sig) {
+            *out = ents[k].exec;
+            if (k) std::swap(ents[k], ents[0]);  // most recent first
+            return AW_OK;
+        }
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(g->s, cudaStreamCaptureModeThreadLocal));
     int64_t dummy = 0;
@@ -659,7 +697,14 @@ aw_status get_graph(aw_grid* g, int G, int cur, cudaGraphExec_t* out) {
     cudaGraphExec_t exec;
     CK(cudaGraphInstantiate(&exec, graph, 0));
     cudaGraphDestroy(graph);
-    g->graphs[key] = exec;
+    // two entries cover aw_set_model's alternating staging arrays; older ones are dropped
+    constexpr size_t kKeep = 3;
+    if (ents.size() >= kKeep) {
+        CK(cudaStreamSynchronize(g->s));  // the dropped graph may still be in flight
+        cudaGraphExecDestroy(ents.back().exec);
+        ents.pop_back();
+    }
+    ents.insert(ents.begin(), aw_grid::GraphEntry{sig, exec});
     *out = exec;
     return AW_OK;
 }
@@ -706,6 +751,24 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
         if ((st = team_prologue(g))) return st;
         g->halo_dirty = false;
     }
+    // AW_OPT_TIMING = 2: the streaming kernel stamps its first-CTA start / last-CTA end per launch
+    // (production path, CUDA graphs kept); the arrays are sized for the run and reset here
+    g->ts_on = g->opt_timing == 2 && g->kernel_used == AW_KERNEL_STREAM && !(g->tb_ready && nt >= 2);
+    if (g->ts_on) {
+        if (g->ts_cap < nt) {
+            const int cap = std::max(nt, 1024);
+            dfree(g, g->ts0);
+            dfree(g, g->ts1);
+            CK(lmalloc(g, (void**)&g->ts0, (size_t)cap * sizeof(unsigned long long)));
+            CK(lmalloc(g, (void**)&g->ts1, (size_t)cap * sizeof(unsigned long long)));
+            g->ts_cap = cap;
+        }
+        CK(cudaMemsetAsync(g->ts0, 0xff, (size_t)g->ts_cap * sizeof(unsigned long long), g->s));
+        CK(cudaMemsetAsync(g->ts1, 0, (size_t)g->ts_cap * sizeof(unsigned long long), g->s));
+        aw::stream_set_timestamps(g->plan, g->ts0, g->ts1, g->ts_cap);
+    } else if (g->plan) {
+        aw::stream_set_timestamps(g->plan, nullptr, nullptr, 0);
+    }
     CK(cudaEventRecord(g->ev_t0, g->s));
     int64_t base = g->steps;
     CK(cudaMemcpyAsync(g->d_base, &base, sizeof base, cudaMemcpyHostToDevice, g->s));
@@ -717,7 +780,7 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
 // Enqueue the nt steps.  Direct launches (with per-stencil events when
 // timing) or graphs of G steps.
 aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
-    const bool timing = g->opt_timing != 0;
+    const bool timing = g->opt_timing == 1;  // per-launch events (direct launches); 2 = device timestamps
     const int G = g->opt_graph;
     if (timing && (int64_t)g->tev.size() < 2 * (int64_t)nt) {
         while ((int64_t)g->tev.size() < 2 * (int64_t)nt) {
@@ -815,7 +878,21 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     g->stats.kernel = g->kernel_used;
     if (g->plan) g->eta_tiles_pct = aw::stream_eta_tiles_pct(g->plan);
     g->stats.eta_tiles = g->eta_tiles_pct;
-    if (g->opt_timing) {
+    if (g->ts_on) {
+        std::vector<unsigned long long> t0(g->ts_cap), t1(g->ts_cap);
+        CK(cudaMemcpy(t0.data(), g->ts0, t0.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t1.data(), g->ts1, t1.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        double sum_ns = 0.0;
+        int64_t n = 0;
+        for (int k = 0; k < g->ts_cap; ++k)
+            if (t1[k] != 0 && t0[k] != ~0ull && t1[k] >= t0[k]) {
+                sum_ns += (double)(t1[k] - t0[k]);
+                ++n;
+            }
+        g->stats.ms_stencil = sum_ns * 1e-6;
+        g->stats.n_stencil = n;
+        g->stats.timed_launches = n;
+    } else if (g->opt_timing == 1) {
         double sum = 0.0;
         for (int i = 0; i < g->n_timed; ++i) {
             float e = 0.f;
@@ -1074,6 +1151,8 @@ void aw_grid_destroy(aw_grid* g) {
         }
     dfree(g, g->dense_lib);
     dfree(g, g->ctl);
+    dfree(g, g->ts0);
+    dfree(g, g->ts1);
     for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
     if (g->ev_sync) cudaEventDestroy(g->ev_sync);
     if (g->ev_t0) cudaEventDestroy(g->ev_t0);
@@ -1296,7 +1375,6 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
     aw_status st = enter(g);
     if (st) return st;
     free_receivers(g);
-    free_graphs(g);
     if (nr == 0) return leave(g);
     g->nr = nr;
     g->rec_nt = nt_max;
@@ -1704,7 +1782,8 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
             free_graphs(g);
             return AW_OK;
         case AW_OPT_TIMING:
-            g->opt_timing = value != 0;
+            if (value < 0 || value > 2) return fail(AW_EINVAL, "timing option must be 0, 1 or 2");
+            g->opt_timing = (int)value;  // graphs captured with/without the timestamp arrays differ in signature
             return AW_OK;
         case AW_OPT_GRAPH_STEPS:
             if (value < 0 || value > 4096) return fail(AW_EINVAL, "graph steps out of range");
@@ -1918,14 +1997,15 @@ aw_status aw_team_run(aw_grid** grids, int world, int nt, double dt) {
     for (int i = 0; i < nt; ++i) {
         for (int r = 0; r < world; ++r) {
             aw_grid* g = grids[r];
-            if (g->opt_timing && (int64_t)g->tev.size() < 2 * (int64_t)nt) {
+            if (g->opt_timing == 1 && (int64_t)g->tev.size() < 2 * (int64_t)nt) {
                 while ((int64_t)g->tev.size() < 2 * (int64_t)nt) {
                     cudaEvent_t e;
                     CK(cudaEventCreate(&e));
                     g->tev.push_back(e);
                 }
             }
-            cudaEvent_t e0 = g->opt_timing ? g->tev[2 * i] : nullptr, e1 = g->opt_timing ? g->tev[2 * i + 1] : nullptr;
+            const bool ev = g->opt_timing == 1;
+            cudaEvent_t e0 = ev ? g->tev[2 * i] : nullptr, e1 = ev ? g->tev[2 * i + 1] : nullptr;
             CK(cudaSetDevice(g->device));
             aw_status st = enqueue_step(g, i, g->cur, e0, e1, &launches[r]);
             if (st) return st;

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <string>
+
 #define AW_MAXR 8          // space order <= 16
 #define AW_PITCH_ALIGN 32  // x pitch in floats (128 B rows: coalescing + TMA 16-B strides)
 
@@ -118,6 +120,10 @@ cudaError_t stream_refresh(StreamPlan* p, const Geom& g, const float* const* ubu
 int stream_eta_tiles_pct(const StreamPlan* p);
 void stream_release(StreamPlan* p);
 size_t stream_plan_bytes(const StreamPlan* p);  // device bytes the plan holds (NULL -> 0)
+// appends every plan value a captured launch uses (tensor maps, tables, timestamps) to *sig
+void stream_plan_signature(const StreamPlan* p, std::string* sig);
+// AW_OPT_TIMING = 2: point the streaming kernel at per-launch timestamp arrays (null = off)
+void stream_set_timestamps(StreamPlan* p, unsigned long long* ts0, unsigned long long* ts1, int cap);
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
                                   const float* ucur, float* unext, const float* b, const float* a,
                                   const Halo& halo, int parity_next, const Sparse& sp, const int64_t* d_base,

@@ -123,6 +123,30 @@ int stream_eta_tiles_pct(const StreamPlan* p) {
     return p->nflags ? (int)(100.0 * (double)h / (double)p->nflags + 0.5) : 0;
 }
 
+void stream_plan_signature(const StreamPlan* p, std::string* sig) {
+    if (!p) return;
+    auto put = [&](const void* q, size_t n) { sig->append((const char*)q, n); };
+    put(p->maps, sizeof p->maps);
+    put(&p->flags, sizeof p->flags);
+    put(p->tpsc, sizeof p->tpsc);
+    put(p->tpe, sizeof p->tpe);
+    put(&p->grid, sizeof p->grid);
+    put(&p->ntx, sizeof p->ntx);
+    put(&p->nty, sizeof p->nty);
+    put(&p->nzc, sizeof p->nzc);
+    put(&p->zc, sizeof p->zc);
+    put(&p->ts0, sizeof p->ts0);
+    put(&p->ts1, sizeof p->ts1);
+    put(&p->ts_cap, sizeof p->ts_cap);
+}
+
+void stream_set_timestamps(StreamPlan* p, unsigned long long* ts0, unsigned long long* ts1, int cap) {
+    if (!p) return;
+    p->ts0 = ts0;
+    p->ts1 = ts1;
+    p->ts_cap = ts0 ? cap : 0;
+}
+
 size_t stream_plan_bytes(const StreamPlan* p) {
     if (!p) return 0;
     size_t n = p->flags ? (size_t)p->nflags + sizeof(unsigned long long) + 16 : 0;

@@ -197,7 +197,19 @@ struct StreamArgs {
     const float* ucur;       // u^n buffer base (plane -R)
     const int64_t* d_base;   // the step index is n = *d_base + step_i (graph-replay friendly)
     int step_i;
+    // device-clock timing on the production path (AW_OPT_TIMING = 2, CUDA graphs kept): the first
+    // CTA start and the last CTA end of launch n go to ts0[n % ts_cap] (atomicMin) and
+    // ts1[n % ts_cap] (atomicMax), %globaltimer ns; null when off
+    unsigned long long* ts0;
+    unsigned long long* ts1;
+    int ts_cap;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct StreamMaps {
     CUtensorMap u;    // u^n buffer, box (TXP, TYP, 1): ring loads + L2 prefetch
@@ -442,6 +454,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const int ntiles = A.ntx * A.nty;
 
     const int64_t step_n = *A.d_base + A.step_i;
+    const int ts_slot = A.ts0 ? (int)(step_n % A.ts_cap) : 0;
+    if (A.ts0 && tid == 0) atomicMin(A.ts0 + ts_slot, globaltimer_ns());
     if (warp == C::NWARPS_COMP + 2) {
         // ---------------- receivers warp: rec[n][r] = fma chain of u^n corners --------
         for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
@@ -453,9 +467,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             }
             A.traces[step_n * A.nr + A.rec_id[r]] = acc;
         }
-        return;
-    }
-    if (warp >= C::NWARPS_COMP) {
+    } else if (warp >= C::NWARPS_COMP) {
         // ---------------- producer warps ----------------
         // warp NWARPS_COMP: u^n plane tiles (with halo) into the ring, D planes ahead, and L2
         // prefetches PD planes ahead; warp NWARPS_COMP+1: the u^{n-1}, b, a tiles of the output
@@ -513,23 +525,26 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 }
             }
         }
-        return;
+    } else {
+        // ---------------- consumer warps ----------------
+        const int ly = warp * C::RY;  // first tile row of this thread
+        Ring ru{0, 0}, rp{0, 0};
+        for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+            const int tile = item % ntiles;
+            const int zb = (item / ntiles) * A.zc;
+            const int ze = min(nz, zb + A.zc);
+            const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+            if (x0 + TX <= g.nx && y0 + TY <= g.ny)
+                consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
+                                            lane, ly, ru, rp, step_n, A.unext);
+            else
+                consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
+                                             lane, ly, ru, rp, step_n, A.unext);
+        }
     }
-
-    // ---------------- consumer warps ----------------
-    const int ly = warp * C::RY;  // first tile row of this thread
-    Ring ru{0, 0}, rp{0, 0};
-    for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
-        const int tile = item % ntiles;
-        const int zb = (item / ntiles) * A.zc;
-        const int ze = min(nz, zb + A.zc);
-        const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
-        if (x0 + TX <= g.nx && y0 + TY <= g.ny)
-            consume_item<C, true, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane, ly,
-                                        ru, rp, step_n, A.unext);
-        else
-            consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0, lane,
-                                         ly, ru, rp, step_n, A.unext);
+    if (A.ts0) {  // this CTA's end: every role done
+        __syncthreads();
+        if (tid == 0) atomicMax(A.ts1 + ts_slot, globaltimer_ns());
     }
 }
 
@@ -794,6 +809,10 @@ struct StreamPlan {
     // tensor maps of explicit-buffer launches (FWI history ring, adjoint pair), keyed by
     // (base pointer, box kind); cleared when the plan is refreshed
     std::unordered_map<uint64_t, CUtensorMap> map_cache;
+    // AW_OPT_TIMING = 2: per-launch device timestamps (buffers owned by the grid handle; null = off)
+    unsigned long long* ts0 = nullptr;
+    unsigned long long* ts1 = nullptr;
+    int ts_cap = 0;
 };
 
 namespace {
@@ -905,6 +924,9 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.ucur = ucur;
     A.d_base = d_base;
     A.step_i = step_i;
+    A.ts0 = p->ts0;
+    A.ts1 = p->ts1;
+    A.ts_cap = p->ts_cap;
     if (A.lo || A.hi)
         stream_kernel<C, true><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
     else
@@ -964,6 +986,9 @@ cudaError_t launch_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const floa
     A.ucur = ucur;
     A.d_base = d_base;
     A.step_i = step_i;
+    A.ts0 = p->ts0;
+    A.ts1 = p->ts1;
+    A.ts_cap = p->ts_cap;
     stream_kernel<C, false><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, A);
     return cudaGetLastError();
 }

@@ -49,7 +49,7 @@ def test_sm100a_code_in_library(aw):
 
 
 def test_abi_version_and_critical_dt(aw):
-    assert aw.aw_abi_version() == 1
+    assert aw.aw_abi_version() == 2
     from tests import _indep
     for k in (2, 4, 8, 12, 16):
         for sp in ([10.0, 10.0], [10.0, 7.0, 12.0]):
