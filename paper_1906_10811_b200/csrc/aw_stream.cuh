@@ -131,12 +131,19 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
-template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_, bool ADJ_ = true>
+template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_, bool ADJ_ = true, int CREG_ = 0,
+          int PREG_ = 40>
 struct Cfg {
     static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
     // lane -> columns: ADJ = the adjacent pair (2l, 2l+1), read and written with 64-bit shared/global
     // accesses; otherwise (l, l+32) with 32-bit accesses (the round-1 mapping, kept for A/B runs)
     static constexpr bool ADJ = ADJ_;
+    // CREG > 0: warpgroup layout -- the consumer warps form whole warpgroups and the three service
+    // warps (+1 idle) a fourth one; at entry the service warpgroup gives its registers back
+    // (setmaxnreg.dec to PREG) and the consumers grow to CREG (setmaxnreg.inc).  The register file
+    // then holds more consumer warps than a uniform allocation would (the service warps need few).
+    static constexpr int CREG = CREG_, PREG = PREG_;
+    static constexpr bool WG = CREG_ > 0;
     static constexpr int CA = ADJ ? 2 : 1;   // first column = CA * lane
     static constexpr int CB = ADJ ? 1 : 32;  // second column = first + CB
     static constexpr int Q = 2 * R + 1;  // z queue length (and plane-loop unroll)
@@ -149,7 +156,11 @@ struct Cfg {
     static constexpr int SP = DP + 1;     // (u^{n-1}, b, a) ring of the output planes
     static constexpr int NWARPS_COMP = TY / RY;
     static constexpr int NCOMP = 32 * NWARPS_COMP;
-    static constexpr int NTHREADS = NCOMP + 96;  // + u^n producer, streams producer, receivers warp
+    // + u^n producer, streams producer, receivers warp (+ an idle warp completing the warpgroup)
+    static constexpr int NTHREADS = NCOMP + (WG ? 128 : 96);
+    static_assert(!WG || (NWARPS_COMP % 4 == 0 && NCOMP * CREG + 128 * PREG <= 65536 && CREG % 8 == 0 &&
+                          PREG % 8 == 0 && PREG >= 24 && CREG <= 256),
+                  "warpgroup register split");
     static constexpr int STAGE_FLOATS = TXP * TYP;
     static constexpr int STAGE_BYTES = STAGE_FLOATS * 4;                 // TMA transaction bytes
     static constexpr int STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;  // 128-B aligned ring slots
@@ -231,6 +242,18 @@ struct Ring {
 };
 
 }  // namespace
+
+// WG layout: the service warpgroup shrinks to PREG registers per thread, the consumer warpgroups
+// grow to CREG (setmaxnreg; every warp of a warpgroup executes the same instruction).  Called at
+// the top of each role's branch, so ptxas allocates that branch's code under the new limit.
+template <class C>
+__device__ __forceinline__ void service_regs() {
+    if constexpr (C::WG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::PREG));
+}
+template <class C>
+__device__ __forceinline__ void consumer_regs() {
+    if constexpr (C::WG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::CREG));
+}
 
 // One work item (xy tile, z chunk) for a consumer thread.  INTERIOR tiles need
 // no bounds predicates.  The ring positions advance exactly like the producer's.
@@ -456,7 +479,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const int64_t step_n = *A.d_base + A.step_i;
     const int ts_slot = A.ts0 ? (int)(step_n % A.ts_cap) : 0;
     if (A.ts0 && tid == 0) atomicMin(A.ts0 + ts_slot, globaltimer_ns());
-    if (warp == C::NWARPS_COMP + 2) {
+    if (warp == C::NWARPS_COMP + 3) {
+        service_regs<C>();  // idle warp of the service warpgroup (WG layout only)
+    } else if (warp == C::NWARPS_COMP + 2) {
+        service_regs<C>();
         // ---------------- receivers warp: rec[n][r] = fma chain of u^n corners --------
         for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
             float acc = 0.0f;
@@ -468,6 +494,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             A.traces[step_n * A.nr + A.rec_id[r]] = acc;
         }
     } else if (warp >= C::NWARPS_COMP) {
+        service_regs<C>();
         // ---------------- producer warps ----------------
         // warp NWARPS_COMP: u^n plane tiles (with halo) into the ring, D planes ahead, and L2
         // prefetches PD planes ahead; warp NWARPS_COMP+1: the u^{n-1}, b, a tiles of the output
@@ -526,6 +553,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             }
         }
     } else {
+        consumer_regs<C>();
         // ---------------- consumer warps ----------------
         const int ly = warp * C::RY;  // first tile row of this thread
         Ring ru{0, 0}, rp{0, 0};
@@ -661,7 +689,12 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const int nitems = (2 * T.nzc + T.lead) * ntiles;
     const int64_t step_n = *A.d_base + A.step_i;  // the pass advances steps n and n+1
 
+    if (warp == C::NWARPS_COMP + 3) {  // idle warp of the service warpgroup (WG layout)
+        service_regs<C>();
+        return;
+    }
     if (warp == C::NWARPS_COMP + 2) {
+        service_regs<C>();
         // ---- receivers: rec[n] from X (read-only in this pass), rec[n+1] from V once the A items
         // owning its corners completed (they never wait, so this cannot deadlock) ----
         for (int r = blockIdx.x + gridDim.x * lane; r < A.nrl; r += gridDim.x * 32) {
@@ -689,6 +722,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         return;
     }
     if (warp >= C::NWARPS_COMP) {
+        service_regs<C>();
         // ---- producers: as in stream_kernel, with the map pair chosen by the item kind ----
         const bool is_u = warp == C::NWARPS_COMP;
         if (lane == 0) {
@@ -751,6 +785,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     }
 
     // ---- consumers ----
+    consumer_regs<C>();
     const int ly = warp * C::RY;
     const uint64_t st_keep = policy_evict_last(), st_drop = policy_evict_first();
     Ring ru{0, 0}, rp{0, 0};
@@ -1064,6 +1099,11 @@ using C6v3 = Cfg<6, 32, 2, 2, 2, 0, 1>;
 using C8v1 = Cfg<8, 16, 2, 3, 3, 0, 1>;
 using C8v2 = Cfg<8, 16, 1, 4, 4, 0, 1>;  // 16 consumer warps, one row each
 using C8v3 = Cfg<8, 16, 2, 4, 4, 0, 1, false>;
+// warpgroup layout (setmaxnreg): 12 consumer warps, 24-row tiles
+using C6v4 = Cfg<6, 24, 2, 2, 2, 0, 1, true, 152, 40>;
+using C6v5 = Cfg<6, 24, 2, 3, 2, 0, 1, true, 152, 40>;
+using C8v4 = Cfg<8, 24, 2, 2, 2, 0, 1, true, 152, 40>;
+using C8v5 = Cfg<8, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 
 int variant() {
     const char* v = dev_knob("AW_STREAM_VARIANT");

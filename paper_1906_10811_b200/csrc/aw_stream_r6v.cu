@@ -7,6 +7,8 @@ const StreamOps* stream_ops_r6_variant(int v) {
     switch (v) {
         case 1: return ops_of<C6v1>();
         case 2: return ops_of<C6v2>();
+        case 4: return ops_of<C6v4>();
+        case 5: return ops_of<C6v5>();
         default: return ops_of<C6v3>();
     }
 }

@@ -1,0 +1,7 @@
+# round 2 session 2: re-verify the restored tree (GPU suite, smoke, default bench, C5/C4 bench lines)
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err; echo "bench rc $?" >> gpurun_out/bench_C3.err
+timeout 600 python bench.py --workload C5 --no-cpu-baseline > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err
+timeout 900 python bench.py --workload C4 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err
+tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench_C3.json gpurun_out/bench_C5.json gpurun_out/bench_C4.json; tail -3 gpurun_out/bench_C3.err
