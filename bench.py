@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "v1", "stream"])
     ap.add_argument("--temporal", type=int, default=0, choices=[0, 1],
                     help="NEXT-1 temporal blocking: two time steps per launch (single slab, 3D)")
+    ap.add_argument("--resident", default="auto", choices=["auto", "on", "off"],
+                    help="small grids: all time steps of a run in one launch of the resident kernel "
+                         "(AW_OPT_RESIDENT; auto = grids up to 8 Mi points)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=50,
@@ -352,6 +355,8 @@ def main():
     if args.kernel != "auto":
         g.set_option(aw.AW_OPT_KERNEL, {"v1": aw.AW_KERNEL_V1, "stream": aw.AW_KERNEL_STREAM}[args.kernel])
     g.set_option(aw.AW_OPT_TEMPORAL, args.temporal)
+    g.set_option(aw.AW_OPT_RESIDENT, {"auto": aw.AW_RESIDENT_AUTO, "on": aw.AW_RESIDENT_ON,
+                                      "off": aw.AW_RESIDENT_OFF}[args.resident])
 
     import workloads as W
     m_dev, d_dev = local_model(spec, g.z0, g.nz, device)
@@ -490,14 +495,16 @@ def main():
     pts_local = float(g.nz) * float(np.prod(shape[1:]))
     # temporal blocking (NEXT-1): one launch = one two-step pass whose algorithmic traffic is 20 B/pt
     # (read u^n, u^{n-1}, b; write u^{n+1}, u^{n+2}); otherwise one launch = one step at 16 B/pt
-    tb = st["timed_launches"] > 0 and st["timed_launches"] < st["n_stencil"]
+    # (the resident kernel also covers many steps per launch, but one step per pass: per-step time)
+    tb = not st["resident"] and st["timed_launches"] > 0 and st["timed_launches"] < st["n_stencil"]
     steps_per_launch = 2 if tb else 1
     bytes_per_launch_pt = 20 if tb else B_STRICT
     avg_ms = ms_stencil / max(1, n_stencil) * steps_per_launch  # average launch duration (odd tail step ~ half)
     achieved = bytes_per_launch_pt * pts_local / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    kname = ("tb2" if tb else "stream") if st["kernel"] == aw.AW_KERNEL_STREAM else "v1"
+    kname = ("tb2" if tb else "resident" if st["resident"] else "stream") if st["kernel"] == aw.AW_KERNEL_STREAM \
+        else "v1"
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)

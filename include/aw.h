@@ -83,10 +83,17 @@ enum {
                            launch with the streaming kernel (3D, single slab; a third wavefield buffer is
                            allocated); results are bit-identical to one step per launch.  Off by default:
                            measured 6-45 % slower than one step per launch on B200 (NEXT-1) */
-    AW_OPT_FWI_ACCUMULATE = 7 /* value 0/1 (default 0): NEXT-4 multi-shot -- with 1, aw_fwi_gradient writes the
+    AW_OPT_FWI_ACCUMULATE = 7, /* value 0/1 (default 0): NEXT-4 multi-shot -- with 1, aw_fwi_gradient writes the
                            fp32 sum (in call order) of the gradients of all calls since the option was last
                            set; setting it (either value) clears the sum.  J is still per call. */
+    AW_OPT_RESIDENT = 8 /* value AW_RESIDENT_* (default AUTO): small grids -- aw_run advances all nt steps in
+                           ONE launch of the resident streaming kernel (3D, single slab, streaming kernel,
+                           not with temporal blocking or AW_OPT_TIMING=1): every CTA keeps its work items
+                           for all steps and an item starts step n+1 once its 27 neighbouring items
+                           finished step n (no grid barrier, no launch gaps).  Same per-point sequence,
+                           bit-identical results.  AUTO uses it up to 8 Mi points (L2-resident grids). */
 };
+enum { AW_RESIDENT_OFF = 0, AW_RESIDENT_ON = 1 /* whenever supported */, AW_RESIDENT_AUTO = 2 };
 
 /* aw_dist.flags */
 enum { AW_DIST_WORKSPACE = 1 /* the caller provides the device memory of the grid's arrays with
@@ -257,6 +264,7 @@ typedef struct {
     int64_t exchange_waits; /* team: waits that found the neighbour's halo not yet delivered */
     int64_t lib_device_bytes; /* device bytes the library itself holds for this handle (cudaMalloc) */
     int64_t workspace_bytes;  /* bytes of the bound caller workspace (0 = none) */
+    int32_t resident;         /* 1: the last aw_run used the resident multi-step kernel (AW_OPT_RESIDENT) */
 } aw_run_stats;
 
 aw_status aw_last_run_stats(const aw_grid* g, aw_run_stats* out);

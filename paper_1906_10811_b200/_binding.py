@@ -31,6 +31,8 @@ AW_GLOBAL, AW_LOCAL = 0, 1
 AW_KERNEL_AUTO, AW_KERNEL_V1, AW_KERNEL_STREAM, AW_KERNEL_TILE2D = 0, 1, 2, 3
 AW_OPT_KERNEL, AW_OPT_TIMING, AW_OPT_GRAPH_STEPS, AW_OPT_CHECK_FINITE, AW_OPT_CHECKPOINT_STEPS = 1, 2, 3, 4, 5
 AW_OPT_TEMPORAL, AW_OPT_FWI_ACCUMULATE = 6, 7
+AW_OPT_RESIDENT = 8
+AW_RESIDENT_OFF, AW_RESIDENT_ON, AW_RESIDENT_AUTO = 0, 1, 2
 AW_DIST_WORKSPACE = 1
 STATUS_NAMES = {0: "AW_OK", -1: "AW_EINVAL", -2: "AW_ENOMEM", -3: "AW_ECUDA", -4: "AW_ENCCL",
                 -5: "AW_ESTATE", -6: "AW_EUNSUPPORTED", -7: "AW_ENONFINITE"}
@@ -47,7 +49,8 @@ class aw_run_stats(ctypes.Structure):
                 ("kernel", ctypes.c_int), ("eta_tiles", ctypes.c_int), ("launches_total", ctypes.c_int64),
                 ("fwi_steps", ctypes.c_int64), ("fwi_checkpoint", ctypes.c_int), ("timed_launches", ctypes.c_int64),
                 ("ms_exchange", ctypes.c_double), ("exchange_waits", ctypes.c_int64),
-                ("lib_device_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64)]
+                ("lib_device_bytes", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("resident", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

@@ -18,7 +18,7 @@ DEV = os.environ.get("AW_DEV_BUILD", "0") == "1"
 SOURCES = (["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu", "aw_fwi.cu", "aw_stencil2d.cu"]
            + [f"aw_stream_r{r}.cu" for r in range(1, 9)]
            + (["aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"] if DEV else []))
-HEADERS = ["aw_internal.h", "aw_stream.cuh", os.path.join("..", "..", "include", "aw.h")]
+HEADERS = ["aw_internal.h", "aw_stream.cuh", "aw_hstream.cuh", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
@@ -28,6 +28,35 @@ if DEV:
 STAMP = os.path.join(CSRC, ".build_kind")  # "dev" / "product": a switch forces a rebuild
 
 
+OBJDIR = os.path.join(CSRC, "obj-dev" if DEV else "obj")  # per build kind: flags differ
+
+
+def _deps(path: str, seen=None) -> set:
+    """path plus the local headers it includes (recursively)."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for line in open(path, errors="replace"):
+        line = line.strip()
+        if line.startswith("#include \""):
+            inc = os.path.normpath(os.path.join(os.path.dirname(path), line.split('"')[1]))
+            _deps(inc, seen)
+    return seen
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJDIR, src.replace(".cu", ".o"))
+
+
+def _obj_stale(src: str) -> bool:
+    obj = _obj(src)
+    if not os.path.exists(obj) or not os.path.exists(obj + ".log"):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in _deps(os.path.join(CSRC, src)) | {__file__})
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -35,28 +64,34 @@ def _stale() -> bool:
     if not os.path.exists(STAMP) or open(STAMP).read().strip() != kind:
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [__file__]
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(_obj_stale(s) or os.path.getmtime(_obj(s)) > t for s in SOURCES)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    # the translation units compile in parallel (aw_stream.cu dominates: one kernel per R and mode)
+    os.makedirs(OBJDIR, exist_ok=True)
+    # the translation units compile in parallel (one streaming-kernel unit per R); only stale objects
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        if not force and not _obj_stale(src):
+            continue
+        obj = _obj(src)
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
-    objs, logs, errors = [], [], []
+    errors = []
     for src, obj, p in procs:
         out, _ = p.communicate()
-        logs.append(out)
         if p.returncode != 0:
             errors.append(f"nvcc failed for {src}:\n{out}")
-        objs.append(obj)
+            if os.path.exists(obj):
+                os.remove(obj)
+            continue
+        with open(obj + ".log", "w") as f:
+            f.write(out)
     if errors:
         raise RuntimeError("\n".join(errors))
+    objs = [_obj(s) for s in SOURCES]
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -65,7 +100,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, LIB)
     with open(STAMP, "w") as f:
         f.write("dev" if DEV else "product")
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
+    logs = [open(o + ".log").read() for o in objs]
+    with open(os.path.join(CSRC, "ptxas.log" if not DEV else "ptxas-dev.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

@@ -228,6 +228,10 @@ struct aw_grid {
     float* d_Gacc = nullptr;
     // NEXT-1 temporal blocking (two steps per launch): third wavefield buffer, readiness
     int opt_temporal = 0;                  // AW_OPT_TEMPORAL (off: measured slower on B200, DESIGN.md NEXT-1)
+    int opt_resident = AW_RESIDENT_AUTO;   // AW_OPT_RESIDENT (small-grid multi-step kernel)
+    bool resident_used = false;            // the last run used the resident kernel
+    std::vector<int64_t> h_rec_off;        // owned receivers' corner offsets (resident kernel's item lists)
+    bool rec_items_dirty = true;           // h_rec_off changed since the lists were built
     float* ubuf_spare = nullptr;
     bool tb_ready = false;
     int n_timed = 0;                       // timed stencil launches of the last run (AW_OPT_TIMING)
@@ -421,6 +425,9 @@ void build_injection(const aw_grid* g, int n, const std::vector<int64_t>& corner
 // (m, eta, b, a).  aw_set_model swaps the roles of m<->b and eta<->a (staging), so after the first
 // placement the pointers, not the offsets, say which array is which.
 constexpr size_t kDenseAlign = 4096;
+// AW_RESIDENT_AUTO picks the resident multi-step kernel up to this many points (~128 MB at 16 B per
+// point: the working set fits in the 126 MB L2, and a step takes microseconds, so launch gaps matter)
+constexpr int64_t kResidentAutoPoints = 8LL << 20;
 void place_dense(aw_grid* g, char* base) {
     const size_t U = align_up(g->ubytes, kDenseAlign), M = align_up(g->mbytes, kDenseAlign);
     g->dense = base;
@@ -470,6 +477,8 @@ void free_receivers(aw_grid* g) {  // views into g->rec_arena
     g->rec_corner_lin.clear();
     g->rec_w32.clear();
     g->rec_w64.clear();
+    g->h_rec_off.clear();
+    g->rec_items_dirty = true;
     g->adj_valid = false;
 }
 
@@ -751,6 +760,20 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
         if ((st = team_prologue(g))) return st;
         g->halo_dirty = false;
     }
+    // small grids: the resident multi-step kernel (one launch for the run, per-item step counters)
+    const int64_t npts = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
+    g->resident_used = g->kernel_used == AW_KERNEL_STREAM && !team_mode(g) && !(g->tb_ready && nt >= 2) &&
+                       g->opt_timing != 1 &&
+                       (g->opt_resident == AW_RESIDENT_ON ||
+                        (g->opt_resident == AW_RESIDENT_AUTO && npts <= kResidentAutoPoints)) &&
+                       aw::stream_resident_ready(g->plan);
+    if (g->resident_used) {
+        if (g->rec_items_dirty) {
+            CK(aw::stream_set_receivers(g->plan, g->geom, g->h_rec_off.data(), g->nrl, 1 << g->ndim, g->s));
+            g->rec_items_dirty = false;
+        }
+        CK(aw::stream_resident_begin(g->plan, g->s));
+    }
     // AW_OPT_TIMING = 2: the streaming kernel stamps its first-CTA start / last-CTA end per launch
     // (production path, CUDA graphs kept); the arrays are sized for the run and reset here
     g->ts_on = g->opt_timing == 2 && g->kernel_used == AW_KERNEL_STREAM && !(g->tb_ready && nt >= 2);
@@ -826,6 +849,14 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
         free_graphs(g);
         return AW_OK;
     }
+    if (g->resident_used) {
+        // small grids: every step of the run in one launch of the resident kernel
+        CK(aw::launch_stencil_resident(g->plan, g->geom, g->coefs, g->cur, g->ubuf, g->b,
+                                       g->have_damp ? g->a : nullptr, sparse_view(g), g->d_base, 0, nt, g->s));
+        ++*launches;
+        if (nt & 1) g->cur = 1 - g->cur;
+        return AW_OK;
+    }
     int done = 0;
     if (!timing && G > 0) {  // team steps too: their waits and signals read the level from the device
         while (nt - done >= G) {
@@ -876,6 +907,7 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
     g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
     g->stats.kernel = g->kernel_used;
+    g->stats.resident = g->resident_used ? 1 : 0;
     if (g->plan) g->eta_tiles_pct = aw::stream_eta_tiles_pct(g->plan);
     g->stats.eta_tiles = g->eta_tiles_pct;
     if (g->ts_on) {
@@ -890,7 +922,7 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
                 ++n;
             }
         g->stats.ms_stencil = sum_ns * 1e-6;
-        g->stats.n_stencil = n;
+        g->stats.n_stencil = g->resident_used ? (n > 0 ? nt : 0) : n;  // time steps the timed launches cover
         g->stats.timed_launches = n;
     } else if (g->opt_timing == 1) {
         double sum = 0.0;
@@ -1403,6 +1435,8 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
         }
     }
     g->nrl = (int)ids.size();
+    g->h_rec_off = offs;
+    g->rec_items_dirty = true;
     Packer pk;
     const size_t o_id = pk.add(ids), o_off = pk.add(offs), o_w = pk.add(ws);
     const size_t small = pk.off;
@@ -1669,6 +1703,7 @@ aw_status aw_fwi_gradient(aw_grid* g, int nt, double dt, const float* d_obs, flo
     g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
     g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
     g->stats.kernel = g->kernel_used;
+    g->stats.resident = 0;
     g->stats.fwi_steps = steps_done;
     // the traces of the forward run stay readable; the wavefield levels hold the adjoint field
     g->steps = nt;
@@ -1803,6 +1838,10 @@ aw_status aw_set_option(aw_grid* g, int option, int64_t value) {
             if (value < 0 || value > 1) return fail(AW_EINVAL, "accumulate option must be 0 or 1");
             g->opt_accum = (int)value;
             g->acc_valid = false;  // setting the option (either value) clears the sum
+            return AW_OK;
+        case AW_OPT_RESIDENT:
+            if (value < AW_RESIDENT_OFF || value > AW_RESIDENT_AUTO) return fail(AW_EINVAL, "bad resident option");
+            g->opt_resident = (int)value;
             return AW_OK;
         case AW_OPT_CHECKPOINT_STEPS:
             if (value < 0 || value > (1 << 30)) return fail(AW_EINVAL, "checkpoint steps out of range");

@@ -145,6 +145,18 @@ cudaError_t launch_stencil_tb(StreamPlan* p, const Geom& g, const Coefs& c, cons
                               cudaStream_t s);
 // re-encode the per-parity maps after the caller permuted its wavefield buffers
 cudaError_t stream_remap(StreamPlan* p, const Geom& g, const float* const* ubuf, const float* b, const float* a);
+// Small grids: the resident multi-step kernel (single slab).  stream_resident_ready: the plan's
+// configuration has it and all its CTAs fit on the device at once.  stream_set_receivers: the owned
+// receivers grouped by the work item holding their base corner (rec_off: [nrl][nc] element offsets
+// into a wavefield buffer, as in Sparse; synchronises s).  stream_resident_begin: reset the per-item
+// step counters (once per run, before its first resident launch).
+bool stream_resident_ready(const StreamPlan* p);
+cudaError_t stream_set_receivers(StreamPlan* p, const Geom& g, const int64_t* rec_off, int nrl, int nc,
+                                 cudaStream_t s);
+cudaError_t stream_resident_begin(StreamPlan* p, cudaStream_t s);
+cudaError_t launch_stencil_resident(StreamPlan* p, const Geom& g, const Coefs& c, int cur0, float* const* buf,
+                                    const float* b, const float* a, const Sparse& sp, const int64_t* d_base,
+                                    int step0, int nsteps, cudaStream_t s);
 
 // 2D tiled kernel (aw_stencil2d.cu): one CTA per 64x32 tile, TMA halo box, packed fp32 on column
 // pairs; explicit buffers (in place when uprev == unext).  Sparse work stays in launch_sparse_step.

@@ -72,12 +72,16 @@ cudaError_t stream_prepare(const Geom& g, const float* const* ubuf, const float*
     // when possible), chunks no thinner than 4R planes (warm-up overhead 2R/zc)
     const int ntiles = p->ntx * p->nty;
     int nzc = 1;
-    while ((int64_t)ntiles * nzc < 8LL * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
+    // (the high-order kernel, zq > 1: >= 6 items per CTA -- every item start pays 2R warm-up planes)
+    const int64_t per_cta = p->zq > 1 ? 6 : 8;
+    while ((int64_t)ntiles * nzc < per_cta * p->grid && g.nz / (nzc * 2) >= 4 * g.R) nzc *= 2;
     if (const char* zc_env = dev_knob("AW_STREAM_ZC")) {  // development knob: planes per z chunk
         const int zc = atoi(zc_env);
         if (zc > 0) nzc = (g.nz + zc - 1) / zc;
     }
     p->zc = (g.nz + nzc - 1) / nzc;
+    if (p->zq > 1 && !dev_knob("AW_STREAM_ZC"))  // the high-order kernel's full chunks: multiples of 2R+1
+        p->zc = std::min(g.nz, (p->zc + p->zq - 1) / p->zq * p->zq);
     p->nzc = (g.nz + p->zc - 1) / p->zc;
     const int64_t nflags = (int64_t)ntiles * g.nz;
     if ((e = cudaMalloc(&p->flags, nflags + sizeof(unsigned long long) + 16)) != cudaSuccess) {
@@ -138,6 +142,7 @@ void stream_plan_signature(const StreamPlan* p, std::string* sig) {
     put(&p->ts0, sizeof p->ts0);
     put(&p->ts1, sizeof p->ts1);
     put(&p->ts_cap, sizeof p->ts_cap);
+    put(p->item_inj, sizeof p->item_inj);
 }
 
 void stream_set_timestamps(StreamPlan* p, unsigned long long* ts0, unsigned long long* ts1, int cap) {
@@ -153,7 +158,10 @@ size_t stream_plan_bytes(const StreamPlan* p) {
     for (int k = 0; k < 2; ++k) {
         if (p->tpsc[k]) n += (size_t)p->nflags * sizeof(int2);
         n += p->tpe_cap[k] * sizeof(int4);
+        if (p->item_inj[k]) n += (size_t)p->ntx * p->nty * p->nzc;
     }
+    if (p->res_done) n += (size_t)p->ntx * p->nty * p->nzc * sizeof(unsigned long long);
+    n += p->ritem_cap * sizeof(int);
     if (p->tb_done) n += (size_t)p->tb_nzc * p->ntx * p->nty * sizeof(unsigned long long);
     return n;
 }
@@ -164,7 +172,10 @@ void stream_release(StreamPlan* p) {
     for (int k = 0; k < 2; ++k) {
         if (p->tpsc[k]) cudaFree(p->tpsc[k]);
         if (p->tpe[k]) cudaFree(p->tpe[k]);
+        if (p->item_inj[k]) cudaFree(p->item_inj[k]);
     }
+    if (p->res_done) cudaFree(p->res_done);
+    if (p->ritem) cudaFree(p->ritem);
     if (p->tb_done) cudaFree(p->tb_done);
     delete p;
 }
@@ -194,7 +205,24 @@ cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const
                      [](const std::pair<int64_t, int4>& a, const std::pair<int64_t, int4>& b) { return a.first < b.first; });
     std::vector<int2> tpsc_h;  // only the touched keys are uploaded; the rest is zero (count 0)
     if ((e = cudaMemsetAsync(tpsc, 0, ntp * sizeof(int2), s)) != cudaSuccess) return e;
+    // per work item (tile, z chunk): does it hold injection corners of this set (the high-order
+    // kernel runs those items on its generic path)
+    const int64_t nitems = (int64_t)ntiles * p->nzc;
+    uint8_t*& item_inj = p->item_inj[set];
+    if (!item_inj && (e = cudaMalloc(&item_inj, nitems)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(item_inj, 0, nitems, s)) != cudaSuccess) return e;
     if (ents.empty()) return cudaSuccess;
+    std::vector<int64_t> inj_items;
+    for (const auto& en : ents) {
+        const int64_t tile = en.first / g.nz, z = en.first % g.nz;
+        const int64_t item = (z / p->zc) * ntiles + tile;
+        if (inj_items.empty() || inj_items.back() != item) inj_items.push_back(item);
+    }
+    std::sort(inj_items.begin(), inj_items.end());
+    inj_items.erase(std::unique(inj_items.begin(), inj_items.end()), inj_items.end());
+    static const uint8_t one_byte = 1;  // (pageable source: the copy is staged before the call returns)
+    for (int64_t it : inj_items)
+        if ((e = cudaMemcpyAsync(item_inj + it, &one_byte, 1, cudaMemcpyHostToDevice, s))) return e;
     if (tpe_cap < ents.size()) {
         if (tpe) cudaFree(tpe);
         tpe = nullptr;
@@ -219,6 +247,55 @@ cudaError_t stream_set_injection(StreamPlan* p, const Geom& g, int64_t z0, const
     for (size_t k = 0; k < keys.size(); ++k)
         if ((e = cudaMemcpyAsync(tpsc + keys[k], &vals[k], sizeof(int2), cudaMemcpyHostToDevice, s))) return e;
     return cudaStreamSynchronize(s);  // the host staging vectors die here
+}
+
+bool stream_resident_ready(const StreamPlan* p) {
+    const StreamOps* ops = p ? stream_ops(p->R) : nullptr;
+    return ops && ops->launch_res && p->res_ok;
+}
+
+cudaError_t stream_set_receivers(StreamPlan* p, const Geom& g, const int64_t* rec_off, int nrl, int nc,
+                                 cudaStream_t s) {
+    const int ntiles = p->ntx * p->nty;
+    const int64_t nitems = (int64_t)ntiles * p->nzc;
+    std::vector<int> cnt(nitems + 1, 0), item_of(nrl);
+    for (int r = 0; r < nrl; ++r) {
+        const int64_t off = rec_off[(int64_t)r * nc];  // the base corner (never skipped)
+        const int z = (int)(off / g.plane) - g.R;
+        const int64_t rem = off % g.plane;
+        const int y = (int)(rem / g.pitch), x = (int)(rem % g.pitch);
+        const int it = (z / p->zc) * ntiles + (y / p->TY) * p->ntx + x / p->TX;
+        item_of[r] = it;
+        ++cnt[it + 1];
+    }
+    std::vector<int> h(nitems + 1 + nrl);
+    for (int64_t i = 0; i < nitems; ++i) cnt[i + 1] += cnt[i];
+    for (int64_t i = 0; i <= nitems; ++i) h[i] = cnt[i];
+    for (int r = 0; r < nrl; ++r) h[nitems + 1 + cnt[item_of[r]]++] = r;  // ascending r within an item
+    cudaError_t e;
+    if (p->ritem_cap < h.size()) {
+        if (p->ritem) cudaFree(p->ritem);
+        p->ritem = nullptr;
+        p->ritem_cap = 0;
+        if ((e = cudaMalloc(&p->ritem, h.size() * sizeof(int)))) return e;
+        p->ritem_cap = h.size();
+    }
+    if (!p->res_done && (e = cudaMalloc(&p->res_done, nitems * sizeof(unsigned long long)))) return e;
+    if ((e = cudaMemcpyAsync(p->ritem, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, s))) return e;
+    return cudaStreamSynchronize(s);  // the host staging vector dies here
+}
+
+cudaError_t stream_resident_begin(StreamPlan* p, cudaStream_t s) {
+    if (!p || !p->res_done) return cudaErrorNotSupported;
+    return cudaMemsetAsync(p->res_done, 0, (size_t)p->ntx * p->nty * p->nzc * sizeof(unsigned long long), s);
+}
+
+cudaError_t launch_stencil_resident(StreamPlan* p, const Geom& g, const Coefs& c, int cur0, float* const* buf,
+                                    const float* b, const float* a, const Sparse& sp, const int64_t* d_base,
+                                    int step0, int nsteps, cudaStream_t s) {
+    const StreamOps* ops = p ? stream_ops(p->R) : nullptr;
+    if (!ops || !ops->launch_res) return cudaErrorNotSupported;
+    return ops->launch_res(p, g, c, cur0, buf, b, a, sp, d_base, step0, nsteps, s);
 }
 
 cudaError_t launch_stencil_stream(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur,

@@ -214,6 +214,9 @@ struct StreamArgs {
     unsigned long long* ts0;
     unsigned long long* ts1;
     int ts_cap;
+    // per work item: 1 if it holds injection corners (the split high-order kernel, aw_hstream.cuh,
+    // runs those items on its generic path)
+    const uint8_t* item_inj;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -578,6 +581,231 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 
 
 // ---------------------------------------------------------------------------
+// Small grids: the resident multi-step kernel.  One launch advances nsteps time
+// steps.  Every CTA keeps its work items (item = blockIdx.x + j * gridDim.x) for all steps and runs
+// them step-major with the stream_kernel roles (TMA producers, consumers, fused sparse work); there is
+// no grid-wide barrier: an item starts local step i once the 27 items around it (xy tiles +-1, z
+// chunks +-1 -- a superset of its halo region and of its receivers' corners) have completed step
+// i-1 (per-item counters, release/acquire).  That also orders the in-place write of u^{i+1} over
+// u^{i-1}: the neighbours that read those points as halo at step i-1 are done with it.  Launch
+// gaps disappear and a region can run ahead of a slower one -- the bound for grids that fit in L2,
+// where a step takes microseconds.  Deadlock-free: every CTA is resident and an item at step i
+// waits only for items at step i-1, which every CTA processes first.
+// Receivers are read per item (the item holding the receiver's base corner) by the receivers warp,
+// after the item's wait; the item's completion is published only after those reads (a named
+// barrier with the consumers), so u^i is neither stale nor already overwritten.
+// ---------------------------------------------------------------------------
+struct ResMaps {
+    StreamMaps m[2];  // by the parity of the buffer holding u^n
+};
+
+struct ResArgs {
+    StreamArgs s;               // geometry, coefficients, eta flags, injection lists, receivers
+    float* buf[2];              // the two wavefield buffers (plane -R)
+    int cur0;                   // buffer holding u^n at the launch's first step
+    int nsteps;                 // steps in this launch
+    int step0;                  // local index (within the run) of the first step
+    unsigned long long* done;   // [nitems]: local steps completed (reset per run)
+    const int* ritem_ptr;       // [nitems + 1]: receivers (indices into the owned list) by item
+    const int* ritem_idx;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_epoch(const unsigned long long* p, unsigned long long epoch) {
+    while (ld_acquire_u64(p) < epoch) __nanosleep(64);
+}
+__device__ __forceinline__ void publish_done(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// lanes 0..26 each wait for one neighbour item (the item itself included) to reach `need`
+__device__ __forceinline__ void wait_neighbours(const StreamArgs& A, const unsigned long long* done, int tile, int c,
+                                                unsigned long long need, int lane) {
+    if (need > 0 && lane < 27) {
+        const int tx = tile % A.ntx + lane % 3 - 1, ty = tile / A.ntx + (lane / 3) % 3 - 1, cc = c + lane / 9 - 1;
+        if (tx >= 0 && tx < A.ntx && ty >= 0 && ty < A.nty && cc >= 0 && cc < A.nzc) {
+            const unsigned long long* p = done + (int64_t)cc * A.ntx * A.nty + (int64_t)ty * A.ntx + tx;
+            while (ld_acquire_u64(p) < need) {
+            }
+        }
+    }
+    __syncwarp();
+    // generic-proxy stores of other CTAs (and of this one) -> this CTA's async-proxy (TMA) reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
+    resident_kernel(const __grid_constant__ ResMaps RM, const __grid_constant__ ResArgs RA) {
+    constexpr int R = C::R, TX = C::TX, TY = C::TY, RP = C::RP, SU = C::SU, SP = C::SP, PD = C::PD;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* ring = reinterpret_cast<float*>(smem);
+    float* pring = reinterpret_cast<float*>(smem + C::U_BYTES);
+    uint64_t* fullU = reinterpret_cast<uint64_t*>(smem + C::U_BYTES + C::P_BYTES);
+    uint64_t* emptyU = fullU + SU;
+    uint64_t* fullP = emptyU + SU;
+    uint64_t* emptyP = fullP + SP;
+    int* pmeta = reinterpret_cast<int*>(smem + C::META_OFF);
+    const StreamArgs& A = RA.s;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < SU; ++s) {
+            mbar_init(&fullU[s], 1);
+            mbar_init(&emptyU[s], C::NCOMP);
+        }
+        for (int s = 0; s < SP; ++s) {
+            mbar_init(&fullP[s], 1);
+            mbar_init(&emptyP[s], C::NCOMP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const Geom& g = A.g;
+    const int nz = g.nz;
+    const int ntiles = A.ntx * A.nty;
+    const int64_t base = *A.d_base;
+    const int ts_slot = A.ts0 ? (int)((base + RA.step0) % A.ts_cap) : 0;
+    if (A.ts0 && tid == 0) atomicMin(A.ts0 + ts_slot, globaltimer_ns());
+    if (warp == C::NWARPS_COMP + 2) {
+        // ---------------- receivers warp: per item, once its neighbours finished the
+        // previous step, rec[n][r] = fma chain of the u^n corners of the item's receivers; the item's
+        // consumers publish its completion only after this warp reached named barrier 2 ----------
+        for (int t = 0; t < RA.nsteps; ++t) {
+            const int i = RA.step0 + t;
+            const float* ucur = RA.buf[RA.cur0 ^ (t & 1)];
+            const int64_t step_n = base + i;
+            for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+                const int e0 = RA.ritem_ptr[item], e1 = RA.ritem_ptr[item + 1];
+                if (e1 > e0) {
+                    wait_neighbours(A, RA.done, item % ntiles, item / ntiles, (unsigned long long)i, lane);
+                    for (int e = e0 + lane; e < e1; e += 32) {
+                        const int r = RA.ritem_idx[e];
+                        float acc = 0.0f;
+                        for (int beta = 0; beta < A.nc; ++beta) {
+                            const int64_t off = A.rec_off[(int64_t)r * A.nc + beta];
+                            if (off < 0) continue;
+                            acc = __fmaf_rn(A.rec_w[(int64_t)r * A.nc + beta], __ldcg(ucur + off), acc);
+                        }
+                        A.traces[step_n * A.nr + A.rec_id[r]] = acc;
+                    }
+                    __syncwarp();
+                }
+                // the reads above happen before the item's completion is published; bar.sync (not arrive):
+                // this warp must not run ahead of the consumers by a barrier generation
+                __threadfence_block();
+                asm volatile("bar.sync 2, %0;" ::"r"(C::NCOMP + 32) : "memory");
+            }
+        }
+    } else if (warp == C::NWARPS_COMP) {
+        // ---------------- u^n producer warp: per item, wait for the neighbours (all lanes), then lane 0
+        // streams the u^n plane tiles into the ring ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&RM.m[0].u) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&RM.m[1].u) : "memory");
+        }
+        Ring rr{0, 0};
+        for (int t = 0; t < RA.nsteps; ++t) {
+            const int i = RA.step0 + t;
+            const int par = RA.cur0 ^ (t & 1);
+            const CUtensorMap* mu = &RM.m[par].u;
+            for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+                const int tile = item % ntiles, c = item / ntiles;
+                const int zb = c * A.zc;
+                const int ze = min(nz, zb + A.zc);
+                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+                const int niter = ze - zb + 2 * R;
+                wait_neighbours(A, RA.done, tile, c, (unsigned long long)i, lane);
+                if (lane == 0) {
+                    for (int kk = 0; kk < PD && kk < niter; ++kk) tma_prefetch_l2_3d(mu, x0 - RP, y0 - R, zb + kk);
+                    for (int k = 0; k < niter; ++k) {
+                        if (k + PD < niter) tma_prefetch_l2_3d(mu, x0 - RP, y0 - R, zb + k + PD);
+                        mbar_wait(&emptyU[rr.slot], rr.phase ^ 1);
+                        mbar_expect_tx(&fullU[rr.slot], C::STAGE_BYTES);
+                        tma_load_3d(ring + rr.slot * C::STAGE_STRIDE_F, mu, &fullU[rr.slot], x0 - RP, y0 - R, zb + k);
+                        rr.advance(SU);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == C::NWARPS_COMP + 1) {
+        // ---------------- streams producer: u^{n-1}, b, a tiles of the output planes ----------------
+        if (lane == 0) {
+            Ring rr{0, 0};
+            for (int t = 0; t < RA.nsteps; ++t) {
+                const int i = RA.step0 + t;
+                const int par = RA.cur0 ^ (t & 1);
+                const StreamMaps& M = RM.m[par];
+                for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+                    const int tile = item % ntiles;
+                    const int zb = (item / ntiles) * A.zc;
+                    const int ze = min(nz, zb + A.zc);
+                    const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+                    // u^{n-1} of the item: written by its own step i-2 (this CTA's consumers)
+                    if (i >= 2) wait_epoch(RA.done + item, (unsigned long long)(i - 1));
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    for (int z = zb; z < ze; ++z) {
+                        const bool use_a = A.a && A.flags[(int64_t)tile * nz + z];
+                        const int2 tp = A.tpsc ? A.tpsc[(int64_t)tile * nz + z] : make_int2(0, 0);
+                        float* dst = pring + rr.slot * C::PSTAGE_FLOATS;
+                        mbar_wait(&emptyP[rr.slot], rr.phase ^ 1);
+                        pmeta[4 * rr.slot] = use_a;
+                        pmeta[4 * rr.slot + 1] = tp.x;
+                        pmeta[4 * rr.slot + 2] = tp.y;
+                        mbar_expect_tx(&fullP[rr.slot], (use_a ? 3 : 2) * C::PTILE_BYTES);
+                        tma_load_3d(dst, &M.un, &fullP[rr.slot], x0, y0, z + R);
+                        tma_load_3d(dst + C::PTILE_FLOATS, &M.b, &fullP[rr.slot], x0, y0, z);
+                        if (use_a) tma_load_3d(dst + 2 * C::PTILE_FLOATS, &M.a, &fullP[rr.slot], x0, y0, z);
+                        rr.advance(SP);
+                    }
+                }
+            }
+        }
+    } else {
+        // ---------------- consumer warps ----------------
+        const int ly = warp * C::RY;
+        Ring ru{0, 0}, rp{0, 0};
+        for (int t = 0; t < RA.nsteps; ++t) {
+            const int i = RA.step0 + t;
+            float* out = RA.buf[RA.cur0 ^ (t & 1) ^ 1];
+            const int64_t step_n = base + i;
+            for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
+                const int tile = item % ntiles;
+                const int zb = (item / ntiles) * A.zc;
+                const int ze = min(nz, zb + A.zc);
+                const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
+                if (x0 + TX <= g.nx && y0 + TY <= g.ny)
+                    consume_item<C, true, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
+                                                 y0, lane, ly, ru, rp, step_n, out);
+                else
+                    consume_item<C, false, false>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0,
+                                                  y0, lane, ly, ru, rp, step_n, out);
+                // publish "item completed step i": every consumer's stores and the receivers warp's reads
+                // of u^n (barrier 2), then one release
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                asm volatile("bar.sync 2, %0;" ::"r"(C::NCOMP + 32) : "memory");
+                if (tid == 0) {
+                    __threadfence();
+                    publish_done(RA.done + item, (unsigned long long)(i + 1));
+                }
+            }
+        }
+    }
+    if (A.ts0) {  // this CTA's end: every role done
+        __syncthreads();
+        if (tid == 0) atomicMax(A.ts1 + ts_slot, globaltimer_ns());
+    }
+}
+
+// ---------------------------------------------------------------------------
 // NEXT-1: temporal blocking, two time steps per pass.
 //
 // A pass reads X = u^n (with halo), Y = u^{n-1}, b, a and writes V = u^{n+1} (a third
@@ -644,14 +872,6 @@ __device__ __forceinline__ void tb_decode(int item, int ntiles, int nzc, int Z, 
     }
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void wait_epoch(const unsigned long long* p, unsigned long long epoch) {
-    while (ld_acquire_u64(p) < epoch) __nanosleep(64);
-}
 
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
@@ -848,6 +1068,15 @@ struct StreamPlan {
     unsigned long long* ts0 = nullptr;
     unsigned long long* ts1 = nullptr;
     int ts_cap = 0;
+    // split high-order kernel: z chunks are a multiple of zq planes (its unroll; 1 = any);
+    // item_inj[set][item] = 1 if the item (tile, chunk) holds injection corners of that set
+    int zq = 1;
+    uint8_t* item_inj[2] = {nullptr, nullptr};
+    // small grids: the resident multi-step kernel (per-item step counters, receivers by item)
+    unsigned long long* res_done = nullptr;  // [nitems]
+    int* ritem = nullptr;                    // [nitems + 1] CSR pointers, then the receiver indices
+    size_t ritem_cap = 0;                    // ints allocated in ritem
+    int res_ok = 0;                          // the resident kernel fits the plan's grid (occupancy)
 };
 
 namespace {
@@ -901,6 +1130,14 @@ cudaError_t setup(StreamPlan* p, const Geom& g) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tb, tb_kernel<C>, C::NTHREADS, C::SMEM);
     if (e != cudaSuccess) return e;
     occ = occ < occ_tb ? occ : occ_tb;
+    // the resident kernel too, if it fits: it is used only when all of its CTAs are co-resident
+    int occ_res = 0;
+    if (cudaFuncSetAttribute(resident_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_res, resident_kernel<C>, C::NTHREADS, C::SMEM) ==
+            cudaSuccess)
+        p->res_ok = occ_res >= occ;
+    cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorNotSupported;
     int dev = 0, sms = 0;
@@ -945,6 +1182,7 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.nitems = p->ntx * p->nty * p->nzc;
     A.tpsc = sp.nuc > 0 ? p->tpsc[0] : nullptr;
     A.tpe = p->tpe[0];
+    A.item_inj = sp.nuc > 0 ? p->item_inj[0] : nullptr;
     A.inj_src = sp.inj_src;
     A.inj_s = sp.inj_s;
     A.wavelet = sp.wavelet;
@@ -1007,6 +1245,7 @@ cudaError_t launch_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const floa
     A.nitems = p->ntx * p->nty * p->nzc;
     A.tpsc = sp.nuc > 0 ? p->tpsc[inj_set] : nullptr;
     A.tpe = p->tpe[inj_set];
+    A.item_inj = sp.nuc > 0 ? p->item_inj[inj_set] : nullptr;
     A.inj_src = sp.inj_src;
     A.inj_s = sp.inj_s;
     A.wavelet = sp.wavelet;
@@ -1025,6 +1264,56 @@ cudaError_t launch_bufs(StreamPlan* p, const Geom& g, const Coefs& c, const floa
     A.ts1 = p->ts1;
     A.ts_cap = p->ts_cap;
     stream_kernel<C, false><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, A);
+    return cudaGetLastError();
+}
+
+// One launch of the resident kernel: nsteps steps from local step step0 (single slab).
+template <class C>
+cudaError_t launch_res(StreamPlan* p, const Geom& g, const Coefs& c, int cur0, float* const* buf, const float* b,
+                       const float* a, const Sparse& sp, const int64_t* d_base, int step0, int nsteps,
+                       cudaStream_t s) {
+    if (!p->res_done || !p->ritem || !p->res_ok) return cudaErrorNotSupported;
+    ResMaps M;
+    M.m[0] = p->maps[0];
+    M.m[1] = p->maps[1];
+    ResArgs R;
+    std::memset(&R, 0, sizeof R);
+    StreamArgs& A = R.s;
+    A.g = g;
+    A.c = c;
+    A.a = a;
+    A.flags = p->flags;
+    A.ntx = p->ntx;
+    A.nty = p->nty;
+    A.nzc = p->nzc;
+    A.zc = p->zc;
+    A.nitems = p->ntx * p->nty * p->nzc;
+    A.tpsc = sp.nuc > 0 ? p->tpsc[0] : nullptr;
+    A.tpe = p->tpe[0];
+    A.inj_src = sp.inj_src;
+    A.inj_s = sp.inj_s;
+    A.wavelet = sp.wavelet;
+    A.ns = sp.ns;
+    A.nrl = sp.nrl;
+    A.nr = sp.nr;
+    A.nc = sp.nc;
+    A.rec_id = sp.rec_id;
+    A.rec_off = sp.rec_off;
+    A.rec_w = sp.rec_w;
+    A.traces = sp.traces;
+    A.d_base = d_base;
+    A.ts0 = p->ts0;
+    A.ts1 = p->ts1;
+    A.ts_cap = p->ts_cap;
+    R.buf[0] = buf[0];
+    R.buf[1] = buf[1];
+    R.cur0 = cur0;
+    R.nsteps = nsteps;
+    R.step0 = step0;
+    R.done = p->res_done;
+    R.ritem_ptr = p->ritem;
+    R.ritem_idx = p->ritem + A.nitems + 1;
+    resident_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, R);
     return cudaGetLastError();
 }
 
@@ -1080,10 +1369,10 @@ cudaError_t launch_tb(StreamPlan* p, const Geom& g, const Coefs& c, const float*
 
 // configuration table: (R, TY, RY, D = u^n ring lookahead, DP = streams lookahead,
 //                       PD = L2 prefetch distance, min CTAs/SM)
-using C1 = Cfg<1, 32, 4, 4, 4, 0, 1>;
-using C2 = Cfg<2, 32, 4, 4, 4, 0, 1>;
-using C3 = Cfg<3, 32, 4, 4, 4, 0, 1>;
-using C4 = Cfg<4, 32, 4, 4, 4, 0, 1>;
+using C1 = Cfg<1, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
+using C2 = Cfg<2, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
+using C3 = Cfg<3, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
+using C4 = Cfg<4, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
 using C6 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // 0.52 vs 0.56 ms (TY 32, RY 4, spills) on 512^3 (profiles/r1)
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
@@ -1122,6 +1411,8 @@ struct StreamOps {
                                const float*, const float*, const Sparse&, int, const int64_t*, int, cudaStream_t);
     cudaError_t (*launch_tb)(StreamPlan*, const Geom&, const Coefs&, const float*, float*, float*, const float*,
                              const float*, const Sparse&, const int64_t*, int, cudaStream_t);
+    cudaError_t (*launch_res)(StreamPlan*, const Geom&, const Coefs&, int, float* const*, const float*, const float*,
+                              const Sparse&, const int64_t*, int, int, cudaStream_t);
 };
 const StreamOps* stream_ops_r1();
 const StreamOps* stream_ops_r2();
@@ -1135,7 +1426,7 @@ const StreamOps* stream_ops_r8();
 namespace {
 template <class C>
 const StreamOps* ops_of() {
-    static const StreamOps o{setup<C>, make_maps<C>, launch<C>, launch_bufs<C>, launch_tb<C>};
+    static const StreamOps o{setup<C>, make_maps<C>, launch<C>, launch_bufs<C>, launch_tb<C>, launch_res<C>};
     return &o;
 }
 }  // namespace

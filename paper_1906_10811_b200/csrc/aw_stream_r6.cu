@@ -1,5 +1,6 @@
-// aw_stream_r6.cu -- instantiations of the streaming kernel for R = 6 (space order 12).
-#include "aw_stream.cuh"
+// aw_stream_r6.cu -- instantiations of the streaming kernel for R = 6 (space order 12); dev builds
+// also hold the split high-order kernel (aw_hstream.cuh) on the same plan geometry, for A/B runs.
+#include "aw_hstream.cuh"
 
 namespace aw {
 #ifdef AW_DEV_VARIANTS
@@ -8,7 +9,8 @@ const StreamOps* stream_ops_r6_variant(int v);  // aw_stream_r6v.cu (measurement
 
 const StreamOps* stream_ops_r6() {
 #ifdef AW_DEV_VARIANTS
-    if (const int v = variant()) return stream_ops_r6_variant(v);  // AW_STREAM_VARIANT=1/2/3 (A/B measurements)
+    // AW_STREAM_VARIANT=8: the split high-order kernel (aw_hstream.cuh); 1..5: measurement variants
+    if (const int v = variant()) return v == 8 ? ops_of_h<H6, C6>() : stream_ops_r6_variant(v);
 #endif
     return ops_of<C6>();
 }

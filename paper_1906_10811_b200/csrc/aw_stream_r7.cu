@@ -1,8 +1,12 @@
-// aw_stream_r7.cu -- instantiations of the streaming kernel for R = 7 (space order 14).
-#include "aw_stream.cuh"
+// aw_stream_r7.cu -- instantiations of the streaming kernel for R = 7 (space order 14); dev builds
+// also hold the split high-order kernel (aw_hstream.cuh) on the same plan geometry, for A/B runs.
+#include "aw_hstream.cuh"
 
 namespace aw {
 const StreamOps* stream_ops_r7() {
+#ifdef AW_DEV_VARIANTS
+    if (variant() == 8) return ops_of_h<H7, C7>();  // AW_STREAM_VARIANT=8: the split high-order kernel (A/B)
+#endif
     return ops_of<C7>();
 }
 }  // namespace aw

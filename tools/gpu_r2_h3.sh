@@ -1,0 +1,13 @@
+# round 2: split high-order kernel (A: in-plane part, B: z part + update) -- quick hang guard, checks,
+# A/B against the generic streaming kernel (AW_STREAM_VARIANT=9), ncu of so 16
+DEV=build/libaw_dev.so
+AW_LIBRARY=$DEV timeout 120 python tools/kernel_check.py --R 8 --nt 4 > gpurun_out/h_quick.log 2>&1; rc=$?; echo "quick rc=$rc" >> gpurun_out/h_quick.log
+tail -4 gpurun_out/h_quick.log
+if [ $rc != 0 ]; then exit 1; fi
+AW_LIBRARY=$DEV timeout 600 python tools/kernel_check.py --R 6,7,8 --shapes all > gpurun_out/h_check.log 2>&1; echo "check rc=$?" >> gpurun_out/h_check.log
+tail -2 gpurun_out/h_check.log
+timeout 900 python tools/ab_stream.py --libs old=$DEV@9,new=$DEV --so 12,14,16 --rounds 2 > gpurun_out/ab_h3.jsonl 2>&1
+cat gpurun_out/ab_h3.jsonl
+AW_LIBRARY=$DEV timeout 300 ncu --set full --import-source on --clock-control none -k regex:hstream_kernel --launch-skip 12 -c 1 \
+  -o gpurun_out/hstream7_so16 -f python tools/ab_stream.py --child 16 --nt 10 > gpurun_out/ncu_h16.log 2>&1
+tail -1 gpurun_out/ncu_h16.log
