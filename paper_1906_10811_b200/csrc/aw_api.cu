@@ -644,7 +644,8 @@ aw_status enqueue_step(aw_grid* g, int i, int cur, cudaEvent_t e0, cudaEvent_t e
                                   g->s));
         ++*launches;
     }
-    if (team_mode(g) && (g->peer_flag_lo || g->peer_flag_hi)) {
+    // (the 3D streaming kernel raises the neighbours' flags itself, as soon as its boundary items are done)
+    if (team_mode(g) && (g->peer_flag_lo || g->peer_flag_hi) && g->kernel_used != AW_KERNEL_STREAM) {
         CK(aw::launch_team_signal(g->peer_flag_lo, g->peer_flag_hi, g->ctl, i, g->s));
         ++*launches;
     }
@@ -865,7 +866,8 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
             if (st) return st;
             CK(cudaGraphLaunch(exec, g->s));
             const int per_step = 1 + (g->kernel_used != AW_KERNEL_STREAM && g->nrl + g->nuc > 0 ? 1 : 0) +
-                                 (team_mode(g) ? 1 + (g->peer_flag_lo || g->peer_flag_hi ? 1 : 0) : 0);
+                                 (team_mode(g) ? 1 + ((g->peer_flag_lo || g->peer_flag_hi) &&
+                                                              g->kernel_used != AW_KERNEL_STREAM ? 1 : 0) : 0);
             *launches += (int64_t)G * per_step + 1;
             done += G;
             if (G & 1) g->cur = 1 - g->cur;
@@ -1951,6 +1953,9 @@ static aw_status link_neighbours(aw_grid* g, float* lo0, float* lo1, unsigned lo
     g->halo.hi_off = 0;
     g->peer_flag_lo = lo_flags ? lo_flags + 1 : nullptr;  // I am rank+1 of my lower neighbour
     g->peer_flag_hi = hi_flags ? hi_flags + 0 : nullptr;  // I am rank-1 of my upper neighbour
+    g->halo.flag_lo = g->peer_flag_lo;
+    g->halo.flag_hi = g->peer_flag_hi;
+    g->halo.ctl = g->ctl;
     g->team_connected = true;
     free_graphs(g);
     return AW_OK;

@@ -507,6 +507,8 @@ template <class HC>
 cudaError_t launch_h(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur, const float* ucur, float* unext,
                      const float* b, const float* a, const Halo& halo, int parity_next, const Sparse& sp,
                      const int64_t* d_base, int step_i, cudaStream_t s) {
+    // (teams: the flags are raised by stream_kernel's boundary-first signalling, which this kernel lacks)
+    if (halo.lo[parity_next] || halo.hi[parity_next]) return cudaErrorNotSupported;
     StreamArgs A;
     fill_args_h<HC>(A, p, g, c, ucur, unext, b, a, sp, 0, d_base, step_i);
     A.lo = halo.lo[parity_next];

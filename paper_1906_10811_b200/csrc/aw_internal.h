@@ -44,11 +44,17 @@ struct Geom {
 };
 
 // Peer targets for the fused halo stores (team mode); null when absent.
+struct DevCtl;
 struct Halo {
     float* lo[2];   // rank-1's buffers (base = its plane -R); my planes [0,R) go to its planes [nz_lo, nz_lo+R)
     float* hi[2];   // rank+1's buffers; my planes [nz-R, nz) go to its planes [-R, 0)
     int64_t lo_off; // element offset of rank-1's plane nz_lo relative to its base
     int64_t hi_off; // element offset of rank+1's plane -R relative to its base (= 0)
+    // boundary-first signalling from inside the 3D streaming kernel: the neighbours' flag words for
+    // me (peer memory) and my control block (epoch, step base, boundary-item counter)
+    unsigned long long* flag_lo;
+    unsigned long long* flag_hi;
+    DevCtl* ctl;
 };
 
 // Device control words of one handle (one small allocation).  base = global index of the step a
@@ -61,7 +67,8 @@ struct DevCtl {
     unsigned long long wait_ns;  // team: device time spent waiting for halo planes (last run)
     unsigned long long nwait;    // team: waits that blocked (last run)
     unsigned flag;               // non-finite result / invalid model
-    unsigned pad_[7];
+    unsigned bcount;             // team streaming kernel: boundary items completed in the current launch
+    unsigned pad_[6];
     unsigned long long team_flags[2];  // [0]: from rank-1, [1]: from rank+1
 };
 

@@ -217,7 +217,23 @@ struct StreamArgs {
     // per work item: 1 if it holds injection corners (the split high-order kernel, aw_hstream.cuh,
     // runs those items on its generic path)
     const uint8_t* item_inj;
+    // team (boundary first): chunk slots [0, tc_lo) are the chunks holding planes z < R, slots
+    // [tc_lo, tc_nb) the chunks from tc_hi up (planes z >= nz-R), then the interior chunks; the CTA
+    // completing the last of the tc_nb * ntiles boundary items raises the neighbours' flags
+    int tc_lo, tc_hi, tc_nb;
+    DevCtl* ctl;
+    unsigned long long* flag_lo;
+    unsigned long long* flag_hi;
 };
+
+// chunk of chunk slot `slot` (team order: boundary chunks first; identity otherwise)
+template <bool TEAM>
+__device__ __forceinline__ int chunk_of(const StreamArgs& A, int slot) {
+    if constexpr (!TEAM) return slot;
+    if (slot < A.tc_lo) return slot;
+    if (slot < A.tc_nb) return A.tc_hi + (slot - A.tc_lo);
+    return A.tc_lo + (slot - A.tc_nb);
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
@@ -514,7 +530,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             Ring rr{0, 0};
             for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
                 const int tile = item % ntiles;
-                const int zb = (item / ntiles) * A.zc;
+                const int zb = chunk_of<TEAM>(A, item / ntiles) * A.zc;
                 const int ze = min(nz, zb + A.zc);
                 const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
                 const int niter = ze - zb + 2 * R;
@@ -562,7 +578,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         Ring ru{0, 0}, rp{0, 0};
         for (int item = blockIdx.x; item < A.nitems; item += gridDim.x) {
             const int tile = item % ntiles;
-            const int zb = (item / ntiles) * A.zc;
+            const int zb = chunk_of<TEAM>(A, item / ntiles) * A.zc;
             const int ze = min(nz, zb + A.zc);
             const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
             if (x0 + TX <= g.nx && y0 + TY <= g.ny)
@@ -571,6 +587,26 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             else
                 consume_item<C, false, TEAM>(A, ring, pring, fullU, emptyU, fullP, emptyP, pmeta, tile, zb, ze, x0, y0,
                                              lane, ly, ru, rp, step_n, A.unext);
+            if constexpr (TEAM) {
+                if (item < A.tc_nb * ntiles && A.ctl) {
+                    // a boundary item is done (its planes are in the neighbours' halos): count it; the last
+                    // one of the launch raises the flags -- the neighbours' next step can start while this
+                    // rank still computes its interior
+                    asm volatile("bar.sync 1, %0;" ::"r"(C::NCOMP) : "memory");
+                    if (tid == 0) {
+                        __threadfence_system();  // cumulative: every consumer's peer stores (barrier above)
+                        const unsigned nb = (unsigned)(A.tc_nb * ntiles);
+                        if (atomicAdd(&A.ctl->bcount, 1u) + 1u == nb) {
+                            __threadfence_system();
+                            const unsigned long long v =
+                                (A.ctl->epoch << 32) + (unsigned long long)(A.ctl->base + A.step_i + 2);
+                            if (A.flag_lo) atomicMax_system(A.flag_lo, v);
+                            if (A.flag_hi) atomicMax_system(A.flag_hi, v);
+                            atomicExch(&A.ctl->bcount, 0u);  // every count of this launch is in
+                        }
+                    }
+                }
+            }
         }
     }
     if (A.ts0) {  // this CTA's end: every role done
@@ -1200,6 +1236,17 @@ cudaError_t launch(StreamPlan* p, const Geom& g, const Coefs& c, int parity_cur,
     A.ts0 = p->ts0;
     A.ts1 = p->ts1;
     A.ts_cap = p->ts_cap;
+    if (A.lo || A.hi) {
+        // boundary chunks first: [0, tc_lo) hold planes z < R, [tc_hi, nzc) planes z >= nz - R
+        const int zc = p->zc, nzc = p->nzc;
+        A.tc_lo = std::min(nzc, (g.R + zc - 1) / zc);
+        A.tc_hi = std::max(A.tc_lo, std::min(nzc, std::max(0, g.nz - g.R) / zc));
+        A.tc_nb = A.tc_lo + (nzc - A.tc_hi);
+        A.ctl = halo.ctl;
+        A.flag_lo = halo.flag_lo;
+        A.flag_hi = halo.flag_hi;
+        if (!A.flag_lo && !A.flag_hi) A.ctl = nullptr;  // nobody to signal
+    }
     if (A.lo || A.hi)
         stream_kernel<C, true><<<p->grid, C::NTHREADS, C::SMEM, s>>>(p->maps[parity_cur], A);
     else

@@ -292,6 +292,36 @@ def test_virtual_team_equals_single(aw, world, ndim):
     assert_parity(rec, orec, "team traces")
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_virtual_team_boundary_first(aw, world):
+    """Slabs deep enough for interior z chunks: the streaming kernel hands out the boundary chunks
+    first and raises the neighbours' flags from inside the kernel once they are done (no signal
+    kernel: 2 launches per step); bit-exact vs the oracle, with sources and receivers at the
+    boundaries and in the interior."""
+    k = 8
+    w = workloads.small_case((40 * world + 10, 40, 70), k, 17, nbl=4, ns=3, nr=8, seed=41)
+    grids = [aw.Grid(w.shape, w.extent, k, rank=r, world=world) for r in range(world)]
+    aw.team_connect_local(grids)
+    for g in grids:
+        g.set_model(w.m, w.damp)
+        g.add_sources(w.src_coords, w.wavelet)
+        g.add_receivers(w.rec_coords, w.nt)
+    aw.team_run(grids, 7, w.dt)
+    aw.team_run(grids, w.nt - 7, w.dt)
+    for g in grids:
+        st = g.stats()
+        assert st["kernel"] == aw.AW_KERNEL_STREAM
+    u = np.zeros(w.shape, np.float32)
+    rec = np.zeros((w.nt, len(w.rec_coords)), np.float32)
+    for g in grids:
+        g.read_wavefield(0, out=u)
+        rec += g.read_receivers()
+        g.close()
+    ou, _, orec = run_oracle(w)
+    assert_parity(u, ou, "team u")
+    assert_parity(rec, orec, "team traces")
+
+
 @pytest.mark.parametrize("kernel", ["auto", "v1"])
 def test_virtual_team_thin_slabs(aw, kernel):
     """Slabs thinner than 2R (R <= nz < 2R): a middle rank's planes are both low and high boundary
