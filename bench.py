@@ -504,7 +504,7 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     kname = ("tb2" if tb else "resident" if st["resident"] else "stream") if st["kernel"] == aw.AW_KERNEL_STREAM \
-        else "v1"
+        else ("resident2d" if st["resident"] else "tile2d") if st["kernel"] == aw.AW_KERNEL_TILE2D else "v1"
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)

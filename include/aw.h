@@ -28,8 +28,15 @@
  *    unchanged.  AW_ECUDA is sticky: the handle is poisoned and every later
  *    call except aw_grid_destroy returns AW_ESTATE.
  *  - Calls on one handle are not thread-safe (concurrent reads are
- *    safe, writes require external exclusivity).  All calls are synchronous
- *    with respect to the handle's stream except where stated.
+ *    safe, writes require external exclusivity).  Calls are stream-ordered on
+ *    the handle's stream (aw_dist.stream when given: the library's work waits
+ *    for the work already queued on it, and later work queued on it waits for
+ *    the library's): host inputs are consumed and host outputs are complete
+ *    when a call returns; device-pointer inputs and outputs are read and
+ *    written in that stream order (aw_add_sources, aw_add_receivers, aw_reset
+ *    and aw_read_receivers with device pointers may return before their
+ *    copies ran).  aw_set_model and aw_run return after their work
+ *    completed (their status depends on it).
  *  - There is no CPU fallback: without a usable CUDA device aw_grid_create
  *    returns AW_ECUDA.
  */
@@ -91,7 +98,11 @@ enum {
                            not with temporal blocking or AW_OPT_TIMING=1): every CTA keeps its work items
                            for all steps and an item starts step n+1 once its 27 neighbouring items
                            finished step n (no grid barrier, no launch gaps).  Same per-point sequence,
-                           bit-identical results.  AUTO uses it up to 8 Mi points (L2-resident grids). */
+                           bit-identical results.  AUTO uses it up to 8 Mi points (L2-resident grids).
+                           2D (AUTO kernel, single slab): grids whose two wavefield levels fit one SM's
+                           shared memory (~25 K points, e.g. C1 = 101^2) run all nt steps in ONE launch of
+                           one CTA holding the grid in shared memory (AUTO and ON; also with
+                           AW_OPT_TIMING=1).  Same per-point sequence, bit-identical results. */
 };
 enum { AW_RESIDENT_OFF = 0, AW_RESIDENT_ON = 1 /* whenever supported */, AW_RESIDENT_AUTO = 2 };
 

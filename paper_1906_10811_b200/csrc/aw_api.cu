@@ -114,6 +114,13 @@ struct aw_grid {
     cudaStream_t s = nullptr;
     cudaStream_t ext = nullptr;
     cudaEvent_t ev_sync = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    // pinned host staging of the small uploads (sparse tables): the copies are truly asynchronous; the
+    // event guards the buffer's reuse (the previous upload must have left it)
+    char* h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    cudaEvent_t ev_stage = nullptr;
+    bool stage_pending = false;
+    unsigned model_epoch = 0;  // aw_set_model calls (device-side validation writes the failing epoch)
     bool poisoned = false;
     // device memory.  The dense arrays (2 wavefield levels, m, eta, b, a) live in one block: the
     // library's own allocation (dense_lib) or the caller's workspace (aw_bind_workspace).
@@ -230,6 +237,7 @@ struct aw_grid {
     int opt_temporal = 0;                  // AW_OPT_TEMPORAL (off: measured slower on B200, DESIGN.md NEXT-1)
     int opt_resident = AW_RESIDENT_AUTO;   // AW_OPT_RESIDENT (small-grid multi-step kernel)
     bool resident_used = false;            // the last run used the resident kernel
+    bool resident2d_used = false;          // the last run used the 2D one-CTA resident kernel
     std::vector<int64_t> h_rec_off;        // owned receivers' corner offsets (resident kernel's item lists)
     bool rec_items_dirty = true;           // h_rec_off changed since the lists were built
     float* ubuf_spare = nullptr;
@@ -501,6 +509,28 @@ struct Packer {
     }
 };
 
+// Asynchronous upload of host bytes through the handle's pinned staging buffer (stream-ordered on g->s).
+aw_status upload(aw_grid* g, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return AW_OK;
+    if (g->stage_pending) {  // the previous upload must have left the buffer
+        CK(cudaEventSynchronize(g->ev_stage));
+        g->stage_pending = false;
+    }
+    if (g->h_stage_cap < bytes) {
+        if (g->h_stage) CK(cudaFreeHost(g->h_stage));
+        g->h_stage = nullptr;
+        g->h_stage_cap = 0;
+        const size_t want = std::max<size_t>(bytes + bytes / 2, 4096);
+        CK(cudaHostAlloc((void**)&g->h_stage, want, cudaHostAllocDefault));
+        g->h_stage_cap = want;
+    }
+    std::memcpy(g->h_stage, src, bytes);
+    CK(cudaMemcpyAsync(dst, g->h_stage, bytes, cudaMemcpyHostToDevice, g->s));
+    CK(cudaEventRecord(g->ev_stage, g->s));
+    g->stage_pending = true;
+    return AW_OK;
+}
+
 // slot: 0 = the sources' arena, 1 = the receivers' (placed in the bound workspace when they fit),
 // -1 = an arena that always lives in library memory (FWI)
 aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes, int slot = -1) {
@@ -549,6 +579,7 @@ aw::Sparse sparse_view(const aw_grid* g) {
     sp.inj_ptr = g->d_inj_ptr;
     sp.inj_src = g->d_inj_src;
     sp.inj_s = g->d_inj_s;
+    sp.nent = g->nent;
     sp.wavelet = g->d_wavelet;
     sp.nc = 1 << g->ndim;
     return sp;
@@ -768,6 +799,9 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
                        (g->opt_resident == AW_RESIDENT_ON ||
                         (g->opt_resident == AW_RESIDENT_AUTO && npts <= kResidentAutoPoints)) &&
                        aw::stream_resident_ready(g->plan);
+    // small 2D grids: one CTA holds the grid in shared memory for the whole run
+    g->resident2d_used = g->kernel_used == AW_KERNEL_TILE2D && !team_mode(g) && g->opt_resident != AW_RESIDENT_OFF &&
+                         aw::resident2d_fits(g->geom, sparse_view(g), g->have_damp);
     if (g->resident_used) {
         if (g->rec_items_dirty) {
             CK(aw::stream_set_receivers(g->plan, g->geom, g->h_rec_off.data(), g->nrl, 1 << g->ndim, g->s));
@@ -850,6 +884,16 @@ aw_status run_enqueue(aw_grid* g, int nt, int64_t* launches) {
         free_graphs(g);
         return AW_OK;
     }
+    if (g->resident2d_used) {
+        if (timing) CK(cudaEventRecord(g->tev[0], g->s));
+        CK(aw::launch_stencil_resident2d(g->geom, g->coefs, g->ubuf[g->cur], g->ubuf[1 - g->cur], g->b,
+                                         g->have_damp ? g->a : nullptr, sparse_view(g), g->d_base, 0, nt, g->s));
+        if (timing) CK(cudaEventRecord(g->tev[1], g->s));
+        g->n_timed = timing && nt > 0 ? 1 : 0;
+        *launches += nt > 0 ? 1 : 0;
+        if (nt & 1) g->cur = 1 - g->cur;
+        return AW_OK;
+    }
     if (g->resident_used) {
         // small grids: every step of the run in one launch of the resident kernel
         CK(aw::launch_stencil_resident(g->plan, g->geom, g->coefs, g->cur, g->ubuf, g->b,
@@ -909,7 +953,7 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
     g->stats.points = (int64_t)g->geom.nz * g->geom.ny * g->geom.nx;
     g->stats.gpts = ms > 0 ? (double)g->stats.points * nt / (ms * 1e6) : 0.0;
     g->stats.kernel = g->kernel_used;
-    g->stats.resident = g->resident_used ? 1 : 0;
+    g->stats.resident = g->resident_used || g->resident2d_used ? 1 : 0;
     if (g->plan) g->eta_tiles_pct = aw::stream_eta_tiles_pct(g->plan);
     g->stats.eta_tiles = g->eta_tiles_pct;
     if (g->ts_on) {
@@ -1136,6 +1180,7 @@ aw_status aw_grid_create(aw_grid** out, int ndim, const int64_t* shape, const do
         if (bad(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking), "stream")) break;
         if (bad(cudaEventCreateWithFlags(&g->ev_sync, cudaEventDisableTiming), "event")) break;
         if (bad(cudaEventCreate(&g->ev_t0), "event") || bad(cudaEventCreate(&g->ev_t1), "event")) break;
+        if (bad(cudaEventCreateWithFlags(&g->ev_stage, cudaEventDisableTiming), "event")) break;
         g->ubytes = (size_t)(nz + 2 * R) * G.plane * sizeof(float);
         g->mbytes = (size_t)nz * G.plane * sizeof(float);
         g->dense_bytes = 2 * align_up(g->ubytes, kDenseAlign) + 4 * align_up(g->mbytes, kDenseAlign);
@@ -1191,6 +1236,8 @@ void aw_grid_destroy(aw_grid* g) {
     if (g->ev_sync) cudaEventDestroy(g->ev_sync);
     if (g->ev_t0) cudaEventDestroy(g->ev_t0);
     if (g->ev_t1) cudaEventDestroy(g->ev_t1);
+    if (g->ev_stage) cudaEventDestroy(g->ev_stage);
+    if (g->h_stage) cudaFreeHost(g->h_stage);
     if (g->s) cudaStreamDestroy(g->s);
     cudaGetLastError();
     delete g;
@@ -1319,20 +1366,29 @@ aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout
     float* new_m = g->b;
     float* new_eta = g->a;
     g->coeffs_valid = false;  // b and a are overwritten from here on
-    // padding columns (x >= nx): 0, never read as domain points
-    CK(cudaMemsetAsync(new_m, 0, g->mbytes, g->s));
-    if ((st = copy_in(g, new_m, g->geom.pitch, m + src_off, nx, rows))) return st;
-    if (damp) {
-        CK(cudaMemsetAsync(new_eta, 0, g->mbytes, g->s));
-        if ((st = copy_in(g, new_eta, g->geom.pitch, damp + src_off, nx, rows))) return st;
+    const unsigned epoch = ++g->model_epoch;
+    if (ptr_kind(m) == PK_DEVICE && (!damp || ptr_kind(damp) == PK_DEVICE)) {
+        // device inputs: one kernel copies both arrays into the padded staging layout (padding 0) and
+        // validates them, recording `epoch` in the control block if any value is invalid
+        CK(aw::launch_stage_model(m + src_off, damp ? damp + src_off : nullptr, new_m, damp ? new_eta : nullptr,
+                                  g->geom, &g->ctl->model_bad, epoch, g->s));
+        g->launch_count += 1;
+    } else {
+        // padding columns (x >= nx): 0, never read as domain points
+        CK(cudaMemsetAsync(new_m, 0, g->mbytes, g->s));
+        if ((st = copy_in(g, new_m, g->geom.pitch, m + src_off, nx, rows))) return st;
+        if (damp) {
+            CK(cudaMemsetAsync(new_eta, 0, g->mbytes, g->s));
+            if ((st = copy_in(g, new_eta, g->geom.pitch, damp + src_off, nx, rows))) return st;
+        }
+        CK(aw::launch_validate_model(new_m, damp ? new_eta : nullptr, g->geom, &g->ctl->model_bad, epoch, g->s));
+        g->launch_count += 1;
     }
-    CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
-    CK(aw::launch_validate_model(new_m, damp ? new_eta : nullptr, g->geom, g->d_flag, g->s));
-    g->launch_count += 1;
-    unsigned flag = 0;
-    CK(cudaMemcpyAsync(&flag, g->d_flag, sizeof flag, cudaMemcpyDeviceToHost, g->s));
-    CK(cudaStreamSynchronize(g->s));
+    unsigned bad = 0;
+    CK(cudaMemcpyAsync(&bad, &g->ctl->model_bad, sizeof bad, cudaMemcpyDeviceToHost, g->s));
+    CK(cudaStreamSynchronize(g->s));  // the validation decides the call's status (strong guarantee)
     if ((st = leave(g))) return st;
+    const unsigned flag = bad == epoch;
     if (flag) return fail(AW_EINVAL, "model invalid: m must be finite and > 0, damp finite and >= 0 "
                                      "(the previous model stays in force)");
     std::swap(g->m, g->b);
@@ -1389,10 +1445,16 @@ aw_status aw_add_sources(aw_grid* g, int ns, const double* coords, int nt_max, c
     g->d_inj_w64 = (double*)(A + o_w);
     g->d_inj_s = (float*)(A + o_s);
     g->d_wavelet = (float*)(A + o_wav);
-    CK(cudaMemcpyAsync(A, pk.host.data(), small, cudaMemcpyHostToDevice, g->s));
-    cudaMemcpyKind kind = ptr_kind(wavelet) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpyAsync(g->d_wavelet, wavelet, (size_t)nt_max * ns * sizeof(float), kind, g->s));
-    CK(cudaStreamSynchronize(g->s));
+    if ((st = upload(g, A, pk.host.data(), small))) return st;
+    const size_t wbytes = (size_t)nt_max * ns * sizeof(float);
+    if (ptr_kind(wavelet) == PK_DEVICE) {
+        CK(cudaMemcpyAsync(g->d_wavelet, wavelet, wbytes, cudaMemcpyDeviceToDevice, g->s));  // stream-ordered
+    } else {
+        // host memory: copied before return (a pinned buffer could otherwise change under the DMA)
+        CK(cudaMemcpyAsync(g->d_wavelet, wavelet, wbytes, cudaMemcpyHostToDevice, g->s));
+        CK(cudaStreamSynchronize(g->s));
+        g->stage_pending = false;
+    }
     return leave(g);
 }
 
@@ -1450,9 +1512,8 @@ aw_status aw_add_receivers(aw_grid* g, int nr, const double* coords, int nt_max)
     g->d_rec_off = (int64_t*)(A + o_off);
     g->d_rec_w = (float*)(A + o_w);
     g->d_traces = (float*)(A + o_tr);
-    CK(cudaMemcpyAsync(A, pk.host.data(), small, cudaMemcpyHostToDevice, g->s));
+    if ((st = upload(g, A, pk.host.data(), small))) return st;  // host tables via the pinned staging buffer
     CK(cudaMemsetAsync(g->d_traces, 0, (size_t)nt_max * nr * sizeof(float), g->s));
-    CK(cudaStreamSynchronize(g->s));
     return leave(g);
 }
 
@@ -1733,8 +1794,8 @@ aw_status aw_reset(aw_grid* g) {
         CK(cudaMemcpyAsync(&g->ctl->epoch, &g->epoch, sizeof g->epoch, cudaMemcpyHostToDevice, g->s));
         CK(aw::launch_team_raise(g->peer_flag_lo, g->peer_flag_hi, enc(g, 0), g->s));
         g->launch_count += 1;
+        CK(cudaStreamSynchronize(g->s));  // collective: the neighbours may rely on the raised epoch
     }
-    CK(cudaStreamSynchronize(g->s));
     return leave(g);
 }
 
@@ -1763,9 +1824,12 @@ aw_status aw_read_receivers(aw_grid* g, float* out) {
     aw_status st = enter(g);
     if (st) return st;
     size_t bytes = (size_t)g->steps * g->nr * sizeof(float);
-    cudaMemcpyKind kind = ptr_kind(out) == PK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CK(cudaMemcpyAsync(out, g->d_traces, bytes, kind, g->s));
-    CK(cudaStreamSynchronize(g->s));
+    if (ptr_kind(out) == PK_DEVICE) {
+        CK(cudaMemcpyAsync(out, g->d_traces, bytes, cudaMemcpyDeviceToDevice, g->s));  // stream-ordered
+    } else {
+        CK(cudaMemcpyAsync(out, g->d_traces, bytes, cudaMemcpyDeviceToHost, g->s));
+        CK(cudaStreamSynchronize(g->s));
+    }
     return leave(g);
 }
 

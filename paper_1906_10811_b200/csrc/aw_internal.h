@@ -68,7 +68,8 @@ struct DevCtl {
     unsigned long long nwait;    // team: waits that blocked (last run)
     unsigned flag;               // non-finite result / invalid model
     unsigned bcount;             // team streaming kernel: boundary items completed in the current launch
-    unsigned pad_[6];
+    unsigned model_bad;          // aw_set_model: epoch of the last call whose model failed validation
+    unsigned pad_[5];
     unsigned long long team_flags[2];  // [0]: from rank-1, [1]: from rank+1
 };
 
@@ -89,6 +90,7 @@ struct Sparse {
     const int* inj_ptr;      // [nuc+1]
     const int* inj_src;      // [nent]
     const float* inj_s;      // [nent] fp32 scales
+    int nent;                // injection entries (inj_ptr[nuc])
     const float* wavelet;    // [nt_max][ns]
     int nc;                  // 2^ndim
 };
@@ -96,8 +98,13 @@ struct Sparse {
 // ---- kernels / launchers (aw_kernels.cu) ----
 cudaError_t launch_coeffs(const float* m, const float* eta, float* b, float* a, int64_t n, double dt,
                           cudaStream_t s);
-cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag,
+// invalid value (m <= 0 or non-finite, eta < 0 or non-finite) -> *bad = epoch
+cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* bad, unsigned epoch,
                                   cudaStream_t s);
+// device inputs (C-order, nx contiguous, nz*ny rows): copy into the padded model layout (padding 0) and
+// validate in one pass
+cudaError_t launch_stage_model(const float* m_src, const float* eta_src, float* m_dst, float* eta_dst, const Geom& g,
+                               unsigned* bad, unsigned epoch, cudaStream_t s);
 cudaError_t launch_source_scales(const float* m, const float* eta, const int64_t* moff, const double* w64,
                                  float* s_out, int nent, double dt, cudaStream_t s);
 // uprev = u^{n-1}: unext itself for the in-place two-buffer time loop, or another buffer
@@ -172,6 +179,15 @@ cudaError_t tile2d_prepare(const Geom& g, Tile2DPlan** plan);
 void tile2d_release(Tile2DPlan* p);
 cudaError_t launch_stencil_tile2d(Tile2DPlan* p, const Geom& g, const Coefs& c, const float* ucur, const float* uprev,
                                   float* unext, const float* b, const float* a, cudaStream_t s);
+
+// Small 2D grids (aw_resident2d.cu): every step of a run in one launch of one CTA holding the whole grid in
+// shared memory (single slab).  resident2d_fits: the two wavefield levels and the sparse tables fit (b, a
+// are staged too when they fit, else read from global).  u_cur/u_prev: the buffers holding u^n / u^{n-1} at entry; both
+// levels are written back at the end (the newest in u_cur when nsteps is even, else in u_prev).
+bool resident2d_fits(const Geom& g, const Sparse& sp, bool damp);
+cudaError_t launch_stencil_resident2d(const Geom& g, const Coefs& c, float* u_cur, float* u_prev, const float* b,
+                                      const float* a, const Sparse& sp, const int64_t* d_base, int step0, int nsteps,
+                                      cudaStream_t s);
 
 // ---- NEXT-3 FWI kernels (aw_fwi.cu) ----
 // G += psi * D,  D = fl32(fl32(u1 - 2 u0) + um1), over the owned planes (wavefield layout inputs,

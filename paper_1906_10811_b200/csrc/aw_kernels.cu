@@ -55,7 +55,7 @@ cudaError_t launch_coeffs(const float* m, const float* eta, float* b, float* a, 
 // Model validation: m > 0 finite, eta >= 0 finite at every owned point.
 // flat float4 walk over the padded arrays; x = element index mod pitch (pitch % 4 == 0)
 __global__ void validate_kernel(const float4* __restrict__ m, const float4* __restrict__ eta, int64_t n4, int nx,
-                                int64_t pitch, unsigned* flag) {
+                                int64_t pitch, unsigned* flag, unsigned epoch) {
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const int x = (int)((4 * i) % pitch);
@@ -66,16 +66,50 @@ __global__ void validate_kernel(const float4* __restrict__ m, const float4* __re
         for (int c = 0; c < 4; ++c)
             if (x + c < nx) bad |= !(mv[c] > 0.0f) || !isfinite(mv[c]) || !(ev[c] >= 0.0f) || !isfinite(ev[c]);
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMax(flag, epoch);
 }
 
-cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag,
+cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& g, unsigned* flag, unsigned epoch,
                                   cudaStream_t s) {
     const int64_t n4 = (int64_t)g.nz * g.plane / 4;
     int blocks = (int)((n4 + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    validate_kernel<<<blocks, 256, 0, s>>>((const float4*)m, (const float4*)eta, n4, g.nx, g.pitch, flag);
+    validate_kernel<<<blocks, 256, 0, s>>>((const float4*)m, (const float4*)eta, n4, g.nx, g.pitch, flag, epoch);
+    return cudaGetLastError();
+}
+
+// Copy m (and eta) from dense C-order device arrays into the padded model layout (pitch-padded rows,
+// padding 0) and validate them in the same pass (aw_set_model with device inputs: one launch instead
+// of memsets + 2D copies + the validation kernel).  Thread i covers element i of the padded layout.
+__global__ void stage_model_kernel(const float* __restrict__ ms, const float* __restrict__ es, float* __restrict__ md,
+                                   float* __restrict__ ed, int64_t rows, int nx, int64_t pitch, unsigned* flag,
+                                   unsigned epoch) {
+    bool bad = false;
+    const int64_t n = rows * pitch;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / pitch;
+        const int x = (int)(i - row * pitch);
+        float mv = 0.0f, ev = 0.0f;
+        if (x < nx) {
+            mv = ms[row * nx + x];
+            if (es) ev = es[row * nx + x];
+            bad |= !(mv > 0.0f) || !isfinite(mv) || !(ev >= 0.0f) || !isfinite(ev);
+        }
+        md[i] = mv;
+        if (ed) ed[i] = ev;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMax(flag, epoch);
+}
+
+cudaError_t launch_stage_model(const float* m_src, const float* eta_src, float* m_dst, float* eta_dst, const Geom& g,
+                               unsigned* bad, unsigned epoch, cudaStream_t s) {
+    const int64_t rows = (int64_t)g.nz * g.ny;
+    const int64_t n = rows * g.pitch;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    stage_model_kernel<<<blocks, 256, 0, s>>>(m_src, eta_src, m_dst, eta_dst, rows, g.nx, g.pitch, bad, epoch);
     return cudaGetLastError();
 }
 
