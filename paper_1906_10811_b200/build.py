@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libaw.so")
 DEV = os.environ.get("AW_DEV_BUILD", "0") == "1"
 SOURCES = (["aw_api.cu", "aw_kernels.cu", "aw_stream.cu", "aw_diffusion.cu", "aw_fwi.cu", "aw_stencil2d.cu", "aw_resident2d.cu"]
            + [f"aw_stream_r{r}.cu" for r in range(1, 9)]
-           + (["aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"] if DEV else []))
+           + (["aw_stream_r2v.cu", "aw_stream_r4v.cu", "aw_stream_r6v.cu", "aw_stream_r8v.cu"] if DEV else []))
 HEADERS = ["aw_internal.h", "aw_stream.cuh", "aw_hstream.cuh", os.path.join("..", "..", "include", "aw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -644,6 +644,7 @@ struct ResArgs {
     unsigned long long* done;   // [nitems]: local steps completed (reset per run)
     const int* ritem_ptr;       // [nitems + 1]: receivers (indices into the owned list) by item
     const int* ritem_idx;
+    int skip_wait;              // development measurement only (AW_RES_NOWAIT, dev builds): no cross-item waits
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -758,7 +759,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 const int ze = min(nz, zb + A.zc);
                 const int x0 = (tile % A.ntx) * TX, y0 = (tile / A.ntx) * TY;
                 const int niter = ze - zb + 2 * R;
-                wait_neighbours(A, RA.done, tile, c, (unsigned long long)i, lane);
+                if (!RA.skip_wait) wait_neighbours(A, RA.done, tile, c, (unsigned long long)i, lane);
                 if (lane == 0) {
                     for (int kk = 0; kk < PD && kk < niter; ++kk) tma_prefetch_l2_3d(mu, x0 - RP, y0 - R, zb + kk);
                     for (int k = 0; k < niter; ++k) {
@@ -1360,6 +1361,7 @@ cudaError_t launch_res(StreamPlan* p, const Geom& g, const Coefs& c, int cur0, f
     R.done = p->res_done;
     R.ritem_ptr = p->ritem;
     R.ritem_idx = p->ritem + A.nitems + 1;
+    R.skip_wait = dev_knob("AW_RES_NOWAIT") != nullptr;  // always 0 in the product library
     resident_kernel<C><<<p->grid, C::NTHREADS, C::SMEM, s>>>(M, R);
     return cudaGetLastError();
 }
