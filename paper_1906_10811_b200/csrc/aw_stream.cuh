@@ -132,9 +132,13 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_, bool ADJ_ = true, int CREG_ = 0,
-          int PREG_ = 40>
+          int PREG_ = 40, bool HQ_ = false>
 struct Cfg {
     static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
+    // HQ: half register queue -- only the R planes below the output plane live in registers; the R above
+    // it are read from the u^n ring, which holds them anyway (R LDS per row more, ~R fewer float2
+    // registers per row, plane loop unrolled R times instead of 2R+1)
+    static constexpr bool HQ = HQ_;
     // lane -> columns: ADJ = the adjacent pair (2l, 2l+1), read and written with 64-bit shared/global
     // accesses; otherwise (l, l+32) with 32-bit accesses (the round-1 mapping, kept for A/B runs)
     static constexpr bool ADJ = ADJ_;
@@ -146,7 +150,7 @@ struct Cfg {
     static constexpr bool WG = CREG_ > 0;
     static constexpr int CA = ADJ ? 2 : 1;   // first column = CA * lane
     static constexpr int CB = ADJ ? 1 : 32;  // second column = first + CB
-    static constexpr int Q = 2 * R + 1;  // z queue length (and plane-loop unroll)
+    static constexpr int Q = HQ ? R : 2 * R + 1;  // z queue length (and plane-loop unroll)
     // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
     // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
     static constexpr int RP = (R + 3) / 4 * 4;
@@ -322,10 +326,20 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
             if (k >= niter) break;
             mbar_wait(&fullU[ru.slot], ru.phase);
             const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + CA * lane;
-            // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
+            if constexpr (!C::HQ) {
+                // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
 #pragma unroll
-            for (int i = 0; i < RY; ++i) q[i][uq] = ld2(P + i * TXP);
+                for (int i = 0; i < RY; ++i) q[i][uq] = ld2(P + i * TXP);
+            }
             const uint32_t slotR = ru.slot >= (uint32_t)R ? ru.slot - R : ru.slot + SU - R;  // plane p-R
+            if constexpr (C::HQ) {
+                // warm-up: planes zb-R .. zb-1 (p-R for R <= k < 2R) are the first outputs' lower z neighbours
+                if (k >= R && k < 2 * R) {
+                    const float* Pc = ring + slotR * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + CA * lane;
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) q[i][uq] = ld2(Pc + i * TXP);
+                }
+            }
             if (k >= 2 * R) {
                 const int z = zb + k - 2 * R;  // output plane
                 const float* Qs = ring + slotR * C::STAGE_STRIDE_F + ly * TXP + RP + CA * lane;
@@ -343,7 +357,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
 #pragma unroll
                 for (int i = 0; i < RY; ++i) {
                     const float* row = Qs + (i + R) * TXP;
-                    const float2 uc = q[i][(uq + Q - R) % Q];
+                    const float2 uc = C::HQ ? col[i + R] : q[i][(uq + Q - R) % Q];
                     float2 L = mul2(C0, uc);
                     if constexpr (C::ADJ) {
                         // v[K + k] = columns (2l + 2k, 2l + 2k + 1), k = -K..K: x neighbours of both points
@@ -374,10 +388,20 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
 #pragma unroll
                     for (int j = 1; j <= R; ++j)
                         L = fma2(f2(A.c.C[1][j], A.c.C[1][j]), add2(col[i + R - j], col[i + R + j]), L);
+                    if constexpr (C::HQ) {
+                        // z - j: register slot (uq - j) mod R; z + j: the ring stage of plane p - R + j
 #pragma unroll
-                    for (int j = 1; j <= R; ++j)
-                        L = fma2(f2(A.c.C[0][j], A.c.C[0][j]),
-                                 add2(q[i][(uq + Q - R - j) % Q], q[i][(uq + Q - R + j) % Q]), L);
+                        for (int j = 1; j <= R; ++j) {
+                            const uint32_t sj = slotR + j < (uint32_t)SU ? slotR + j : slotR + j - SU;
+                            const float2 up = ld2(ring + sj * C::STAGE_STRIDE_F + (ly + R + i) * TXP + RP + CA * lane);
+                            L = fma2(f2(A.c.C[0][j], A.c.C[0][j]), add2(q[i][(uq + R - j) % R], up), L);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 1; j <= R; ++j)
+                            L = fma2(f2(A.c.C[0][j], A.c.C[0][j]),
+                                     add2(q[i][(uq + Q - R - j) % Q], q[i][(uq + Q - R + j) % Q]), L);
+                    }
                     const float* pr = Pp + i * TX;
                     const float2 um = ld2(pr);
                     const float2 bb = ld2(pr + C::PTILE_FLOATS);
@@ -387,6 +411,10 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                     const float2 wv = fma2(bb, L, t);
                     const float2 rr = mul2(add2(one, f2(-aa.x, -aa.y)), um);
                     res[i] = fma2(aa, wv, rr);
+                }
+                if constexpr (C::HQ) {  // u^n of the output plane becomes a lower neighbour (slot uq: plane z-R done)
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) q[i][uq] = col[i + R];
                 }
                 mbar_arrive(&emptyP[rp.slot]);  // every consumer thread arrives: no warp sync, no branch
                 rp.advance(SP);
@@ -1423,7 +1451,9 @@ using C2 = Cfg<2, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C3 = Cfg<3, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C4 = Cfg<4, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
-using C6 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // 0.52 vs 0.56 ms (TY 32, RY 4, spills) on 512^3 (profiles/r1)
+// R = 6 (so 12, C4): half register queue + 12 consumer warps (24-row tiles): 0.525 -> 0.461 ms per step on
+// 512^3 (profiles/r2/ab_hq.jsonl, ab_hq2.jsonl); the HQ variants of R = 4, 5, 7, 8 measured slower
+using C6 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, true>;
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
 using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
@@ -1442,6 +1472,17 @@ using C6v4 = Cfg<6, 24, 2, 2, 2, 0, 1, true, 152, 40>;
 using C6v5 = Cfg<6, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 using C8v4 = Cfg<8, 24, 2, 2, 2, 0, 1, true, 152, 40>;
 using C8v5 = Cfg<8, 24, 2, 3, 2, 0, 1, true, 152, 40>;
+// half register queue (HQ): 8 and 12 consumer warps
+using C6v6 = Cfg<6, 16, 2, 4, 4, 0, 1, true, 0, 40, true>;
+using C6v7 = Cfg<6, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
+using C8v6 = Cfg<8, 16, 2, 4, 4, 0, 1, true, 0, 40, true>;
+using C8v7 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
+using C4v4 = Cfg<4, 16, 2, 3, 3, 0, 2, true, 0, 40, true>;   // HQ, 2 CTAs per SM
+using C4v5 = Cfg<4, 32, 2, 4, 4, 0, 1, true, 0, 40, true>;   // HQ, the product tile
+using C5v6 = Cfg<5, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
+using C5v7 = Cfg<5, 32, 2, 3, 3, 0, 1, true, 0, 40, true>;
+using C6v8 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, true>;
+using C7v6 = Cfg<7, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
 
 int variant() {
     const char* v = dev_knob("AW_STREAM_VARIANT");

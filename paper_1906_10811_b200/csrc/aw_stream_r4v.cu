@@ -7,6 +7,8 @@ const StreamOps* stream_ops_r4_variant(int v) {
     switch (v) {
         case 1: return ops_of<C4v1>();
         case 2: return ops_of<C4v2>();
+        case 4: return ops_of<C4v4>();
+        case 5: return ops_of<C4v5>();
         default: return ops_of<C4v3>();
     }
 }

@@ -9,6 +9,9 @@ const StreamOps* stream_ops_r6_variant(int v) {
         case 2: return ops_of<C6v2>();
         case 4: return ops_of<C6v4>();
         case 5: return ops_of<C6v5>();
+        case 6: return ops_of<C6v6>();
+        case 7: return ops_of<C6v7>();
+        case 9: return ops_of<C6v8>();
         default: return ops_of<C6v3>();
     }
 }

@@ -9,6 +9,8 @@ const StreamOps* stream_ops_r8_variant(int v) {
         case 2: return ops_of<C8v2>();
         case 4: return ops_of<C8v4>();
         case 5: return ops_of<C8v5>();
+        case 6: return ops_of<C8v6>();
+        case 7: return ops_of<C8v7>();
         default: return ops_of<C8v3>();
     }
 }
