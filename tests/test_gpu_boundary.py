@@ -143,3 +143,60 @@ def test_exchange_stats(aw):
         assert st["ms_exchange"] >= 0.0 and 0 <= st["exchange_waits"] <= w.nt
         assert st["ms_exchange"] < st["ms_total"] + 1e-3
         g.close()
+
+
+def test_invalid_device_model_keeps_previous_model(aw):
+    """The device-input path of aw_set_model (one copy-and-validate kernel): invalid values anywhere --
+    including the last point -- return AW_EINVAL and leave the previous model in force; a valid device
+    model then replaces it."""
+    import torch
+    w = workloads.small_case((27, 33, 70), 8, 16, nbl=4, ns=2, nr=6)
+    m_dev = torch.from_numpy(w.m).cuda()
+    d_dev = torch.from_numpy(w.damp).cuda()
+    g = aw.Grid(w.shape, w.extent, w.space_order)
+    g.set_model(m_dev, d_dev)
+    g.add_sources(w.src_coords, w.wavelet)
+    g.add_receivers(w.rec_coords, w.nt)
+    bad_last = m_dev.clone()
+    bad_last.view(-1)[-1] = 0.0
+    bad_eta = d_dev.clone()
+    bad_eta.view(-1)[123] = float("inf")
+    for bm, bd in ((bad_last, d_dev), (m_dev, bad_eta), (-m_dev, None)):
+        with pytest.raises(aw.AwError) as ei:
+            g.set_model(bm, bd)
+        assert ei.value.status == aw.AW_EINVAL
+    g.run(w.nt, w.dt)
+    u, rec = g.read_wavefield(0), g.read_receivers()
+    g.close()
+    ou, _, orec = run_oracle(w)
+    assert_parity(u, ou, "u after rejected device models")
+    assert_parity(rec, orec, "traces after rejected device models")
+
+
+def test_stream_ordered_device_inputs(aw):
+    """include/aw.h: device-pointer inputs and outputs are handled in the stream order of the handle's
+    stream (aw_dist.stream).  Overwriting a device wavelet right after aw_add_sources -- on the same
+    stream, without a host synchronisation -- must not change what the library injects, and a device
+    output of aw_read_receivers is complete for work queued after it on that stream."""
+    import torch
+    w = workloads.small_case((30, 26, 66), 4, 20, nbl=3, ns=3, nr=7)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = aw.Grid(w.shape, w.extent, w.space_order, stream=s)
+        m_dev = torch.from_numpy(w.m).cuda()
+        d_dev = torch.from_numpy(w.damp).cuda()
+        wav_dev = torch.from_numpy(w.wavelet).cuda()
+        g.set_model(m_dev, d_dev)
+        g.add_sources(w.src_coords, wav_dev)
+        wav_dev.fill_(1e30)  # queued after the library's copy on the same stream
+        g.add_receivers(w.rec_coords, w.nt)
+        g.run(w.nt, w.dt)
+        traces = torch.empty((w.nt, len(w.rec_coords)), dtype=torch.float32, device="cuda")
+        g.read_receivers(out=traces)
+        copy = traces.clone()  # queued after the library's device-to-device copy
+    s.synchronize()
+    u = g.read_wavefield(0)
+    g.close()
+    ou, _, orec = run_oracle(w)
+    assert_parity(u, ou, "u (stream-ordered inputs)")
+    assert_parity(copy.cpu().numpy(), orec, "traces (stream-ordered device output)")
