@@ -132,13 +132,15 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 template <int R_, int TY_, int RY_, int D_, int DP_, int PD_, int MINB_, bool ADJ_ = true, int CREG_ = 0,
-          int PREG_ = 40, bool HQ_ = false>
+          int PREG_ = 40, int QJ_ = -1>
 struct Cfg {
     static constexpr int R = R_, TX = 64, TY = TY_, RY = RY_, D = D_, DP = DP_, PD = PD_, MINB = MINB_;
-    // HQ: half register queue -- only the R planes below the output plane live in registers; the R above
-    // it are read from the u^n ring, which holds them anyway (R LDS per row more, ~R fewer float2
-    // registers per row, plane loop unrolled R times instead of 2R+1)
-    static constexpr bool HQ = HQ_;
+    // z queue: registers hold the planes z-R .. z+QJ around the output plane z (QJ_ = -1: QJ = R, the full
+    // 2R+1 queue); the upper neighbours z+QJ+1 .. z+R are read from the u^n ring, which holds them anyway
+    // (R-QJ more 64-bit shared loads per row, R-QJ fewer float2 registers per row, shorter unroll).
+    // QJ = 0 is the half register queue (HQ): the R planes below, the output plane pushed after its update.
+    static constexpr int QJ = QJ_ < 0 ? R : QJ_;
+    static constexpr bool HQ = QJ == 0;
     // lane -> columns: ADJ = the adjacent pair (2l, 2l+1), read and written with 64-bit shared/global
     // accesses; otherwise (l, l+32) with 32-bit accesses (the round-1 mapping, kept for A/B runs)
     static constexpr bool ADJ = ADJ_;
@@ -150,7 +152,7 @@ struct Cfg {
     static constexpr bool WG = CREG_ > 0;
     static constexpr int CA = ADJ ? 2 : 1;   // first column = CA * lane
     static constexpr int CB = ADJ ? 1 : 32;  // second column = first + CB
-    static constexpr int Q = HQ ? R : 2 * R + 1;  // z queue length (and plane-loop unroll)
+    static constexpr int Q = HQ ? R : R + QJ + 1;  // z queue length (and plane-loop unroll)
     // x halo rounded up to a multiple of 4 floats: the TMA box row (TX+2RP)*4 B must be a
     // multiple of 32 B on this part (272/304-B rows trap with an illegal instruction).
     static constexpr int RP = (R + 3) / 4 * 4;
@@ -326,12 +328,22 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
             if (k >= niter) break;
             mbar_wait(&fullU[ru.slot], ru.phase);
             const float* P = ring + ru.slot * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + CA * lane;
-            if constexpr (!C::HQ) {
+            if constexpr (C::QJ == R) {
                 // newest plane -> queue slot uq (rotation by renaming: plane p-m sits in slot (uq-m) mod Q)
 #pragma unroll
                 for (int i = 0; i < RY; ++i) q[i][uq] = ld2(P + i * TXP);
             }
             const uint32_t slotR = ru.slot >= (uint32_t)R ? ru.slot - R : ru.slot + SU - R;  // plane p-R
+            if constexpr (!C::HQ && C::QJ < R) {
+                // partial queue: plane p-R+QJ (= z+QJ of the output plane z = p-R) -> slot uq, from the
+                // iteration where it is the first one the queue needs (zb-R at k = R-QJ)
+                if (k >= R - C::QJ) {
+                    const uint32_t sq = slotR + C::QJ < (uint32_t)SU ? slotR + C::QJ : slotR + C::QJ - SU;
+                    const float* Pq = ring + sq * C::STAGE_STRIDE_F + (ly + R) * TXP + RP + CA * lane;
+#pragma unroll
+                    for (int i = 0; i < RY; ++i) q[i][uq] = ld2(Pq + i * TXP);
+                }
+            }
             if constexpr (C::HQ) {
                 // warm-up: planes zb-R .. zb-1 (p-R for R <= k < 2R) are the first outputs' lower z neighbours
                 if (k >= R && k < 2 * R) {
@@ -357,7 +369,7 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
 #pragma unroll
                 for (int i = 0; i < RY; ++i) {
                     const float* row = Qs + (i + R) * TXP;
-                    const float2 uc = C::HQ ? col[i + R] : q[i][(uq + Q - R) % Q];
+                    const float2 uc = C::HQ ? col[i + R] : q[i][(uq + Q - C::QJ) % Q];
                     float2 L = mul2(C0, uc);
                     if constexpr (C::ADJ) {
                         // v[K + k] = columns (2l + 2k, 2l + 2k + 1), k = -K..K: x neighbours of both points
@@ -395,6 +407,19 @@ __device__ __forceinline__ void consume_item(const StreamArgs& A, const float* r
                             const uint32_t sj = slotR + j < (uint32_t)SU ? slotR + j : slotR + j - SU;
                             const float2 up = ld2(ring + sj * C::STAGE_STRIDE_F + (ly + R + i) * TXP + RP + CA * lane);
                             L = fma2(f2(A.c.C[0][j], A.c.C[0][j]), add2(q[i][(uq + R - j) % R], up), L);
+                        }
+                    } else if constexpr (C::QJ < R) {
+                        // plane z+m sits in slot (uq - QJ + m) mod Q for m in [-R, QJ]; above QJ: the ring
+#pragma unroll
+                        for (int j = 1; j <= R; ++j) {
+                            float2 up;
+                            if (j <= C::QJ) {
+                                up = q[i][(uq + Q - C::QJ + j) % Q];
+                            } else {
+                                const uint32_t sj = slotR + j < (uint32_t)SU ? slotR + j : slotR + j - SU;
+                                up = ld2(ring + sj * C::STAGE_STRIDE_F + (ly + R + i) * TXP + RP + CA * lane);
+                            }
+                            L = fma2(f2(A.c.C[0][j], A.c.C[0][j]), add2(q[i][(uq + 2 * Q - C::QJ - j) % Q], up), L);
                         }
                     } else {
 #pragma unroll
@@ -1453,7 +1478,7 @@ using C4 = Cfg<4, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
 // R = 6 (so 12, C4): half register queue + 12 consumer warps (24-row tiles): 0.525 -> 0.461 ms per step on
 // 512^3 (profiles/r2/ab_hq.jsonl, ab_hq2.jsonl); the HQ variants of R = 4, 5, 7, 8 measured slower
-using C6 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, true>;
+using C6 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, 0>;
 using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
 using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
@@ -1473,16 +1498,22 @@ using C6v5 = Cfg<6, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 using C8v4 = Cfg<8, 24, 2, 2, 2, 0, 1, true, 152, 40>;
 using C8v5 = Cfg<8, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 // half register queue (HQ): 8 and 12 consumer warps
-using C6v6 = Cfg<6, 16, 2, 4, 4, 0, 1, true, 0, 40, true>;
-using C6v7 = Cfg<6, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
-using C8v6 = Cfg<8, 16, 2, 4, 4, 0, 1, true, 0, 40, true>;
-using C8v7 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
-using C4v4 = Cfg<4, 16, 2, 3, 3, 0, 2, true, 0, 40, true>;   // HQ, 2 CTAs per SM
-using C4v5 = Cfg<4, 32, 2, 4, 4, 0, 1, true, 0, 40, true>;   // HQ, the product tile
-using C5v6 = Cfg<5, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
-using C5v7 = Cfg<5, 32, 2, 3, 3, 0, 1, true, 0, 40, true>;
-using C6v8 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, true>;
-using C7v6 = Cfg<7, 24, 2, 3, 3, 0, 1, true, 0, 40, true>;
+using C6v0 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // the round-1/2 product configuration (register queue of 2R+1)
+using C6v6 = Cfg<6, 16, 2, 4, 4, 0, 1, true, 0, 40, 0>;
+using C6v7 = Cfg<6, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+using C8v6 = Cfg<8, 16, 2, 4, 4, 0, 1, true, 0, 40, 0>;
+using C8v7 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+using C4v4 = Cfg<4, 16, 2, 3, 3, 0, 2, true, 0, 40, 0>;   // HQ, 2 CTAs per SM
+using C4v5 = Cfg<4, 32, 2, 4, 4, 0, 1, true, 0, 40, 0>;   // HQ, the product tile
+using C5v6 = Cfg<5, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+using C5v7 = Cfg<5, 32, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+using C6v8 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, 0>;
+using C7v6 = Cfg<7, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+// partial queues (z-R .. z+QJ in registers)
+using C8v9 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 2>;
+using C8v10 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 3>;
+using C8v11 = Cfg<8, 16, 2, 4, 4, 0, 1, true, 0, 40, 4>;
+using C7v9 = Cfg<7, 24, 2, 3, 3, 0, 1, true, 0, 40, 2>;
 
 int variant() {
     const char* v = dev_knob("AW_STREAM_VARIANT");

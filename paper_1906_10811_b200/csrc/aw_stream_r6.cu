@@ -10,7 +10,8 @@ const StreamOps* stream_ops_r6_variant(int v);  // aw_stream_r6v.cu (measurement
 const StreamOps* stream_ops_r6() {
 #ifdef AW_DEV_VARIANTS
     // AW_STREAM_VARIANT=8: the split high-order kernel (aw_hstream.cuh); 1..5: measurement variants
-    if (const int v = variant()) return v == 8 ? ops_of_h<H6, C6>() : stream_ops_r6_variant(v);
+    // (the split kernel pairs with the round-1 geometry, 16-row tiles: C6v0)
+    if (const int v = variant()) return v == 8 ? ops_of_h<H6, C6v0>() : stream_ops_r6_variant(v);
 #endif
     return ops_of<C6>();
 }

@@ -12,6 +12,7 @@ const StreamOps* stream_ops_r6_variant(int v) {
         case 6: return ops_of<C6v6>();
         case 7: return ops_of<C6v7>();
         case 9: return ops_of<C6v8>();
+        case 10: return ops_of<C6v0>();
         default: return ops_of<C6v3>();
     }
 }

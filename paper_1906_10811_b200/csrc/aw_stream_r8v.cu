@@ -11,6 +11,9 @@ const StreamOps* stream_ops_r8_variant(int v) {
         case 5: return ops_of<C8v5>();
         case 6: return ops_of<C8v6>();
         case 7: return ops_of<C8v7>();
+        case 9: return ops_of<C8v9>();
+        case 10: return ops_of<C8v10>();
+        case 11: return ops_of<C8v11>();
         default: return ops_of<C8v3>();
     }
 }
