@@ -508,7 +508,10 @@ def main():
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        ent = tj.get(f"{spec['name']}:{kname}")
+        # per-rank traffic of the profiled launch: C3/C5 weak scaling keep the per-rank slab; C4 (strong
+        # scaling) only at N=1
+        base_name = spec["name"].split("(")[0]
+        ent = tj.get(f"{base_name}:{kname}") if (base_name != "C4" or world == 1) else None
         if ent:
             traffic = ent.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peak,

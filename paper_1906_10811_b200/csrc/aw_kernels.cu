@@ -11,6 +11,8 @@
 //   t   = 2 u_p - u^{n-1}_p
 //   w   = fma(b_p, L, t)                                  (b = dt^2/m, division hoisted,
 //   u^{n+1}_p = fma(a_p, w, (1 - a_p) * u^{n-1}_p)         PAPER.md:788-826; a = m/(m+eta dt/2))
+#include <algorithm>
+
 #include "aw_internal.h"
 
 namespace aw {
@@ -81,23 +83,26 @@ cudaError_t launch_validate_model(const float* m, const float* eta, const Geom& 
 
 // Copy m (and eta) from dense C-order device arrays into the padded model layout (pitch-padded rows,
 // padding 0) and validate them in the same pass (aw_set_model with device inputs: one launch instead
-// of memsets + 2D copies + the validation kernel).  Thread i covers element i of the padded layout.
-__global__ void stage_model_kernel(const float* __restrict__ ms, const float* __restrict__ es, float* __restrict__ md,
-                                   float* __restrict__ ed, int64_t rows, int nx, int64_t pitch, unsigned* flag,
-                                   unsigned epoch) {
+// of memsets + 2D copies + the validation kernel).  x = blockIdx.x * 256 + threadIdx.x covers the
+// padded row, blockIdx.y strides over the rows: coalesced, no integer division.
+__global__ void __launch_bounds__(256) stage_model_kernel(const float* __restrict__ ms, const float* __restrict__ es,
+                                                          float* __restrict__ md, float* __restrict__ ed,
+                                                          int64_t rows, int nx, int64_t pitch, unsigned* flag,
+                                                          unsigned epoch) {
     bool bad = false;
-    const int64_t n = rows * pitch;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / pitch;
-        const int x = (int)(i - row * pitch);
-        float mv = 0.0f, ev = 0.0f;
-        if (x < nx) {
-            mv = ms[row * nx + x];
-            if (es) ev = es[row * nx + x];
-            bad |= !(mv > 0.0f) || !isfinite(mv) || !(ev >= 0.0f) || !isfinite(ev);
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x < pitch) {
+#pragma unroll 4
+        for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
+            float mv = 0.0f, ev = 0.0f;
+            if (x < nx) {
+                mv = ms[row * nx + x];
+                if (es) ev = es[row * nx + x];
+                bad |= !(mv > 0.0f) || !isfinite(mv) || !(ev >= 0.0f) || !isfinite(ev);
+            }
+            md[row * pitch + x] = mv;
+            if (ed) ed[row * pitch + x] = ev;
         }
-        md[i] = mv;
-        if (ed) ed[i] = ev;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMax(flag, epoch);
 }
@@ -105,11 +110,10 @@ __global__ void stage_model_kernel(const float* __restrict__ ms, const float* __
 cudaError_t launch_stage_model(const float* m_src, const float* eta_src, float* m_dst, float* eta_dst, const Geom& g,
                                unsigned* bad, unsigned epoch, cudaStream_t s) {
     const int64_t rows = (int64_t)g.nz * g.ny;
-    const int64_t n = rows * g.pitch;
-    int blocks = (int)((n + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    stage_model_kernel<<<blocks, 256, 0, s>>>(m_src, eta_src, m_dst, eta_dst, rows, g.nx, g.pitch, bad, epoch);
+    const int bx = (int)((g.pitch + 255) / 256);
+    int by = (int)std::min<int64_t>(rows, std::max<int64_t>(1, 148 * 16 / bx));
+    if (by < 1) by = 1;
+    stage_model_kernel<<<dim3(bx, by), 256, 0, s>>>(m_src, eta_src, m_dst, eta_dst, rows, g.nx, g.pitch, bad, epoch);
     return cudaGetLastError();
 }
 
