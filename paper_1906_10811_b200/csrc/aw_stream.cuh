@@ -1476,11 +1476,13 @@ using C2 = Cfg<2, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C3 = Cfg<3, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C4 = Cfg<4, 32, 2, 4, 4, 0, 1>;  // 16 consumer warps, 2 rows each
 using C5 = Cfg<5, 32, 4, 3, 3, 0, 1>;
-// R = 6 (so 12, C4): half register queue + 12 consumer warps (24-row tiles): 0.525 -> 0.461 ms per step on
-// 512^3 (profiles/r2/ab_hq.jsonl, ab_hq2.jsonl); the HQ variants of R = 4, 5, 7, 8 measured slower
-using C6 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, 0>;
-using C7 = Cfg<7, 16, 2, 4, 4, 0, 1>;
-using C8 = Cfg<8, 16, 2, 4, 4, 0, 1>;
+// R = 6..8 (so 12-16; C4, C5): half register queue with 4 rows per thread (8 consumer warps, 64 x 32 tiles):
+// the queue's registers pay for the taller row block, which loads each y column once for 4 rows.  On 512^3
+// (ms per step, profiles/r2/ab_half_queue.jsonl): so 12 0.525 -> 0.427, so 14 0.533 -> 0.481, so 16 0.558
+// -> 0.541; the same change measured no gain for R <= 5
+using C6 = Cfg<6, 32, 4, 3, 2, 0, 1, true, 0, 40, 0>;
+using C7 = Cfg<7, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
+using C8 = Cfg<8, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
 // development variants of R=4 (AW_STREAM_VARIANT=1/2/3), for measurements
 using C4v1 = Cfg<4, 32, 4, 4, 4, 0, 1, false>;  // round-1 lane mapping (l, l+32)
 using C4v2 = Cfg<4, 32, 4, 5, 3, 0, 1>;
@@ -1498,7 +1500,9 @@ using C6v5 = Cfg<6, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 using C8v4 = Cfg<8, 24, 2, 2, 2, 0, 1, true, 152, 40>;
 using C8v5 = Cfg<8, 24, 2, 3, 2, 0, 1, true, 152, 40>;
 // half register queue (HQ): 8 and 12 consumer warps
-using C6v0 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // the round-1/2 product configuration (register queue of 2R+1)
+using C6v0 = Cfg<6, 16, 2, 4, 4, 0, 1>;  // the round-1/2 product configurations (register queue of 2R+1)
+using C7v0 = Cfg<7, 16, 2, 4, 4, 0, 1>;
+using C8v0 = Cfg<8, 16, 2, 4, 4, 0, 1>;
 using C6v6 = Cfg<6, 16, 2, 4, 4, 0, 1, true, 0, 40, 0>;
 using C6v7 = Cfg<6, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
 using C8v6 = Cfg<8, 16, 2, 4, 4, 0, 1, true, 0, 40, 0>;
@@ -1509,6 +1513,19 @@ using C5v6 = Cfg<5, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
 using C5v7 = Cfg<5, 32, 2, 3, 3, 0, 1, true, 0, 40, 0>;
 using C6v8 = Cfg<6, 24, 2, 4, 3, 0, 1, true, 0, 40, 0>;
 using C7v6 = Cfg<7, 24, 2, 3, 3, 0, 1, true, 0, 40, 0>;
+// R = 6 HQ: ring depths, taller per-thread row blocks (fewer y-column loads per point)
+using C6v11 = Cfg<6, 24, 2, 5, 3, 0, 1, true, 0, 40, 0>;
+using C6v12 = Cfg<6, 24, 2, 4, 2, 0, 1, true, 0, 40, 0>;
+using C6v13 = Cfg<6, 24, 3, 4, 3, 0, 1, true, 0, 40, 0>;   // 8 consumer warps x 3 rows
+using C6v14 = Cfg<6, 32, 4, 3, 2, 0, 1, true, 0, 40, 0>;   // 8 consumer warps x 4 rows
+// half queue with 4 rows per thread (8 consumer warps, 64 x 32 tiles)
+using C4v6 = Cfg<4, 32, 4, 4, 4, 0, 1, true, 0, 40, 0>;
+using C5v8 = Cfg<5, 32, 4, 3, 3, 0, 1, true, 0, 40, 0>;
+using C6v15 = Cfg<6, 32, 4, 2, 2, 0, 1, true, 0, 40, 0>;
+using C6v16 = Cfg<6, 32, 4, 3, 1, 0, 1, true, 0, 40, 0>;
+using C7v12 = Cfg<7, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
+using C8v12 = Cfg<8, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
+using C8v13 = Cfg<8, 32, 4, 1, 2, 0, 1, true, 0, 40, 0>;
 // partial queues (z-R .. z+QJ in registers)
 using C8v9 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 2>;
 using C8v10 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 3>;

@@ -9,6 +9,7 @@ const StreamOps* stream_ops_r4_variant(int v) {
         case 2: return ops_of<C4v2>();
         case 4: return ops_of<C4v4>();
         case 5: return ops_of<C4v5>();
+        case 6: return ops_of<C4v6>();
         default: return ops_of<C4v3>();
     }
 }

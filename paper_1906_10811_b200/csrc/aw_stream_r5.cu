@@ -4,7 +4,7 @@
 namespace aw {
 const StreamOps* stream_ops_r5() {
 #ifdef AW_DEV_VARIANTS
-    if (const int v = variant()) return v == 6 ? ops_of<C5v6>() : ops_of<C5v7>();  // A/B measurements
+    if (const int v = variant()) return v == 6 ? ops_of<C5v6>() : v == 8 ? ops_of<C5v8>() : ops_of<C5v7>();  // A/B
 #endif
     return ops_of<C5>();
 }

@@ -13,6 +13,12 @@ const StreamOps* stream_ops_r6_variant(int v) {
         case 7: return ops_of<C6v7>();
         case 9: return ops_of<C6v8>();
         case 10: return ops_of<C6v0>();
+        case 11: return ops_of<C6v11>();
+        case 12: return ops_of<C6v12>();
+        case 13: return ops_of<C6v13>();
+        case 14: return ops_of<C6v14>();
+        case 15: return ops_of<C6v15>();
+        case 16: return ops_of<C6v16>();
         default: return ops_of<C6v3>();
     }
 }

@@ -5,9 +5,11 @@
 namespace aw {
 const StreamOps* stream_ops_r7() {
 #ifdef AW_DEV_VARIANTS
-    if (variant() == 8) return ops_of_h<H7, C7>();  // AW_STREAM_VARIANT=8: the split high-order kernel (A/B)
+    if (variant() == 8) return ops_of_h<H7, C7v0>();  // AW_STREAM_VARIANT=8: the split high-order kernel (A/B)
     if (variant() == 6) return ops_of<C7v6>();      // half register queue, 12 consumer warps
     if (variant() == 9) return ops_of<C7v9>();      // partial queue (QJ = 2), 12 consumer warps
+    if (variant() == 12) return ops_of<C7v12>();    // half queue, 4 rows per thread
+    if (variant() == 10) return ops_of<C7v0>();     // the previous product configuration
 #endif
     return ops_of<C7>();
 }

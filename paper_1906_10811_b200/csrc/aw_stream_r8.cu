@@ -10,7 +10,7 @@ const StreamOps* stream_ops_r8_variant(int v);  // aw_stream_r8v.cu (measurement
 const StreamOps* stream_ops_r8() {
 #ifdef AW_DEV_VARIANTS
     // AW_STREAM_VARIANT=8: the split high-order kernel (aw_hstream.cuh); 1..5: measurement variants
-    if (const int v = variant()) return v == 8 ? ops_of_h<H8, C8>() : stream_ops_r8_variant(v);
+    if (const int v = variant()) return v == 8 ? ops_of_h<H8, C8v0>() : stream_ops_r8_variant(v);
 #endif
     return ops_of<C8>();
 }

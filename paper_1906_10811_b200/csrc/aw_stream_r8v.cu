@@ -14,6 +14,9 @@ const StreamOps* stream_ops_r8_variant(int v) {
         case 9: return ops_of<C8v9>();
         case 10: return ops_of<C8v10>();
         case 11: return ops_of<C8v11>();
+        case 12: return ops_of<C8v12>();
+        case 13: return ops_of<C8v13>();
+        case 14: return ops_of<C8v0>();
         default: return ops_of<C8v3>();
     }
 }
