@@ -20,6 +20,8 @@
 #include <vector>
 
 #include "../../include/aw.h"
+#include <cstddef>
+
 #include "aw_internal.h"
 
 using aw::Coefs;
@@ -531,6 +533,25 @@ aw_status upload(aw_grid* g, void* dst, const void* src, size_t bytes) {
     return AW_OK;
 }
 
+// Queue a copy of the device control block into the pinned staging buffer and synchronise the stream:
+// afterwards g->h_stage holds the DevCtl as of the end of the queued work (one round trip).
+aw_status readback_ctl(aw_grid* g) {
+    if (g->stage_pending) {
+        CK(cudaEventSynchronize(g->ev_stage));
+        g->stage_pending = false;
+    }
+    if (g->h_stage_cap < sizeof(aw::DevCtl)) {
+        if (g->h_stage) CK(cudaFreeHost(g->h_stage));
+        g->h_stage = nullptr;
+        g->h_stage_cap = 0;
+        CK(cudaHostAlloc((void**)&g->h_stage, 4096, cudaHostAllocDefault));
+        g->h_stage_cap = 4096;
+    }
+    CK(cudaMemcpyAsync(g->h_stage, g->ctl, sizeof(aw::DevCtl), cudaMemcpyDeviceToHost, g->s));
+    CK(cudaStreamSynchronize(g->s));
+    return AW_OK;
+}
+
 // slot: 0 = the sources' arena, 1 = the receivers' (placed in the bound workspace when they fit),
 // -1 = an arena that always lives in library memory (FWI)
 aw_status ensure_arena(aw_grid* g, char** arena, size_t* cap, size_t bytes, int slot = -1) {
@@ -828,10 +849,8 @@ aw_status run_begin(aw_grid* g, int nt, double dt) {
         aw::stream_set_timestamps(g->plan, nullptr, nullptr, 0);
     }
     CK(cudaEventRecord(g->ev_t0, g->s));
-    int64_t base = g->steps;
-    CK(cudaMemcpyAsync(g->d_base, &base, sizeof base, cudaMemcpyHostToDevice, g->s));
-    CK(cudaMemsetAsync(g->d_flag, 0, sizeof(unsigned), g->s));
-    CK(cudaMemsetAsync(&g->ctl->wait_ns, 0, 2 * sizeof(unsigned long long), g->s));  // wait_ns, nwait
+    CK(aw::launch_run_init(g->ctl, g->steps, g->s));  // step base, NaN flag, exchange-wait counters
+    g->launch_count += 1;
     return AW_OK;
 }
 
@@ -936,11 +955,13 @@ aw_status run_end(aw_grid* g, int nt, int64_t launches) {
         ++launches;
     }
     CK(cudaEventRecord(g->ev_t1, g->s));
-    aw_status st = leave(g);
+    // the control block comes back with the run's own synchronisation (pinned staging, no second
+    // round trip)
+    aw_status st = readback_ctl(g);
     if (st) return st;
-    CK(cudaStreamSynchronize(g->s));
+    if ((st = leave(g))) return st;
     aw::DevCtl ctl;
-    CK(cudaMemcpy(&ctl, g->ctl, sizeof ctl, cudaMemcpyDeviceToHost));
+    std::memcpy(&ctl, g->h_stage, sizeof ctl);
     const unsigned flag = ctl.flag;
     g->stats.ms_exchange = (double)ctl.wait_ns * 1e-6;
     g->stats.exchange_waits = (int64_t)ctl.nwait;
@@ -1384,9 +1405,9 @@ aw_status aw_set_model(aw_grid* g, const float* m, const float* damp, int layout
         CK(aw::launch_validate_model(new_m, damp ? new_eta : nullptr, g->geom, &g->ctl->model_bad, epoch, g->s));
         g->launch_count += 1;
     }
+    if ((st = readback_ctl(g))) return st;  // the validation decides the call's status (strong guarantee)
     unsigned bad = 0;
-    CK(cudaMemcpyAsync(&bad, &g->ctl->model_bad, sizeof bad, cudaMemcpyDeviceToHost, g->s));
-    CK(cudaStreamSynchronize(g->s));  // the validation decides the call's status (strong guarantee)
+    std::memcpy(&bad, g->h_stage + offsetof(aw::DevCtl, model_bad), sizeof bad);
     if ((st = leave(g))) return st;
     const unsigned flag = bad == epoch;
     if (flag) return fail(AW_EINVAL, "model invalid: m must be finite and > 0, damp finite and >= 0 "

@@ -116,6 +116,7 @@ cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucu
                                const int64_t* d_base, int i, const Halo& halo, int parity_next,
                                cudaStream_t s);
 cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s);
+cudaError_t launch_run_init(DevCtl* ctl, int64_t base, cudaStream_t s);
 cudaError_t launch_check_finite(const Geom& g, const float* u, const float* traces, int64_t t0,
                                 int64_t t1, int nr, unsigned* flag, cudaStream_t s);
 cudaError_t launch_team_wait(DevCtl* ctl, bool has_lo, bool has_hi, int i, cudaStream_t s);

@@ -266,6 +266,20 @@ cudaError_t launch_sparse_step(const Geom& g, const Sparse& sp, const float* ucu
 
 __global__ void advance_kernel(int64_t* d_base, int64_t by) { *d_base += by; }
 
+// start of an aw_run: step base, cleared NaN flag and exchange-wait counters in one launch (instead of a
+// pageable host-to-device copy and two memsets)
+__global__ void run_init_kernel(DevCtl* ctl, int64_t base) {
+    ctl->base = base;
+    ctl->flag = 0u;
+    ctl->wait_ns = 0ull;
+    ctl->nwait = 0ull;
+}
+
+cudaError_t launch_run_init(DevCtl* ctl, int64_t base, cudaStream_t s) {
+    run_init_kernel<<<1, 1, 0, s>>>(ctl, base);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_advance(int64_t* d_base, int64_t by, cudaStream_t s) {
     advance_kernel<<<1, 1, 0, s>>>(d_base, by);
     return cudaGetLastError();
