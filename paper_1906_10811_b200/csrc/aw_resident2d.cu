@@ -14,9 +14,10 @@
 //   * the thread that owns a source corner adds the CSR-ordered injection to the value it just
 //     computed (corner ascending, source ascending: Q11) before storing it,
 //   * a strip's first and last R rows are also stored straight into the neighbouring CTAs' ghost
-//     rows (distributed shared memory: the halo exchange fused into the update, as in the 3D team
-//     kernel), and
-//   * one cluster barrier (release/acquire) separates step n from step n+1,
+//     rows with st.async (distributed shared memory: the halo exchange fused into the update, as in
+//     the 3D team kernel), each store counting its bytes on the receiving CTA's mbarrier, and
+//   * step n+1 starts after a CTA barrier and the two neighbours' halo bytes of step n arrived (per-side,
+//     per-step-parity mbarriers; no cluster-wide barrier or GPU-scope fence per step),
 // and finally each CTA writes both levels of its strip back to the wavefield buffers (restart /
 // aw_read_wavefield see exactly what the per-step kernels would have left).  No HBM traffic per
 // step (traces aside): a step costs one pass over ~1 column pair per thread plus the cluster
@@ -54,7 +55,7 @@ constexpr int kR2MaxCluster = 8;
 struct R2Plan {
     int CS, nzl_max;
     int Ps, C0, slen;
-    int o_b, o_a, o_rsi, o_rw, o_rid, o_ip, o_iptr, o_isrc, o_is, o_wav, o_tr;
+    int o_b, o_a, o_rsi, o_rw, o_rid, o_ip, o_iptr, o_isrc, o_is, o_wav, o_tr, o_mb;
     int words;
 };
 
@@ -109,6 +110,8 @@ R2Plan r2_plan(const Geom& g, const Sparse& sp, bool damp, int CS) {
     o += sp.nuc > 0 ? kR2WavRows * sp.ns : 0;
     P.o_tr = o;
     o += kR2WavRows * sp.nrl;
+    P.o_mb = (o + 1) / 2 * 2;  // 4 mbarriers (8-byte aligned): ghost rows from below / above, by step parity
+    o = P.o_mb + 8;
     P.words = o;
     return P;
 }
@@ -117,12 +120,50 @@ __device__ __forceinline__ float2 ld2s(const float* p) { return *reinterpret_cas
 // cluster barrier with release/acquire at cluster scope: orders the shared-memory (local and
 // distributed) stores of a step before the neighbours' reads of the next one.  (cg's cluster.sync()
 // adds a GPU-scope MEMBAR that also waits for the trace stores to global memory.)
+__device__ __forceinline__ uint32_t smem_u32a(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// asynchronous store into a neighbour CTA's shared memory that counts its bytes on that CTA's mbarrier
+__device__ __forceinline__ void st_async2(uint32_t addr, float2 v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "f"(v.x), "f"(v.y), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async1(uint32_t addr, float v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v),
+                 "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32a(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32a(bar)), "r"(bytes) : "memory");
+}
+// wait for the phase with the given parity; acquire at cluster scope (the bytes came from another CTA)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32a(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void cluster_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <int R, bool DAMP>
+// AS (default): the halo rows go to the neighbours with st.async, each CTA waits only for its two
+// neighbours' bytes (per-side, per-step-parity mbarriers) -- no cluster-wide barrier and no GPU-scope
+// fence per step; !AS: plain DSMEM stores + one cluster barrier per step (kept for A/B runs)
+template <int R, bool DAMP, bool AS>
 __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args A) {
     extern __shared__ __align__(16) float smem[];
     cg::cluster_group cl = cg::this_cluster();
@@ -210,7 +251,14 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
     const float* Bs = smem + P.o_b;
     const float* As = smem + P.o_a;
     const float2 c0 = f2(A.c.C0, A.c.C0), two = f2(2.0f, 2.0f), one = f2(1.0f, 1.0f);
-    // every CTA has loaded its strip before any neighbour stores into its ghost rows
+    // mb[0 + parity]: ghost rows from the CTA below (its last R rows), mb[2 + parity]: from the CTA above
+    uint64_t* mb = reinterpret_cast<uint64_t*>(smem + P.o_mb);
+    const uint32_t side_bytes = (uint32_t)R * A.nx * 4u;
+    if (AS && tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init1(&mb[i]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // every CTA has loaded its strip (and initialised its barriers) before any neighbour stores into it
     cluster_barrier();
 
     // trace rows [n_first, n_first + rows) of this CTA's receivers from the chunk buffer to global memory
@@ -223,6 +271,10 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
     // one time step: U = u^n, W = u^{n-1} in / u^{n+1} out (in place); s = local step index
     auto step = [&](const float* __restrict__ U, float* __restrict__ W, int s) {
         const int64_t n = n0 + s;
+        if (AS && tid == 0) {  // this step's halo bytes from each neighbour (the one arrival of the phase)
+            if (has_dn) mbar_expect(&mb[0 + (s & 1)], side_bytes);
+            if (has_up) mbar_expect(&mb[2 + (s & 1)], side_bytes);
+        }
         if (s % kR2WavRows == 0 && (sp.nuc > 0 || sp.nrl > 0)) {
             // chunk start: the previous chunk's trace rows go to global memory (the GPU-scope fence of the
             // cluster barrier then waits for these stores once per chunk, not every step), and the next
@@ -247,6 +299,14 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
         }
         float* W_dn = has_dn ? cl.map_shared_rank(W, cr - 1) : W;  // the neighbours' copies of this level
         float* W_up = has_up ? cl.map_shared_rank(W, cr + 1) : W;
+        // st.async targets: the neighbours' ghost rows of W and their barriers for this step (the CTA below
+        // receives from above: its mb[2 + parity]; the CTA above: its mb[0 + parity])
+        // (map W's own base -- a valid local address -- then shift in 32-bit arithmetic: W + shift_up lies
+        // below this CTA's window, only W + shift_up + o of a boundary row is inside the neighbour's)
+        const uint32_t wa_dn = has_dn ? mapa_u32(smem_u32a(W), cr - 1) + 4u * (uint32_t)shift_dn : 0u;
+        const uint32_t wa_up = has_up ? mapa_u32(smem_u32a(W), cr + 1) + 4u * (uint32_t)shift_up : 0u;
+        const uint32_t mb_dn = has_dn ? mapa_u32(smem_u32a(&mb[2 + (s & 1)]), cr - 1) : 0u;
+        const uint32_t mb_up = has_up ? mapa_u32(smem_u32a(&mb[0 + (s & 1)]), cr + 1) : 0u;
         int xp = xp_start, zl = zl_start, o = o_start, ob = ob_start;
 #pragma unroll 2
         for (int k = 0; k < kcount; ++k) {
@@ -315,8 +375,17 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
                 else base[o] = un.x;
             };
             put(W);
-            if (has_dn && zl < R) put(W_dn + shift_dn);
-            if (has_up && zl >= nzl - R) put(W_up + shift_up);
+            if constexpr (AS) {
+                auto put_async = [&](uint32_t wa, uint32_t mbr) {
+                    if (pair) st_async2(wa + 4u * (uint32_t)o, un, mbr);
+                    else st_async1(wa + 4u * (uint32_t)o, un.x, mbr);
+                };
+                if (has_dn && zl < R) put_async(wa_dn, mb_dn);
+                if (has_up && zl >= nzl - R) put_async(wa_up, mb_up);
+            } else {
+                if (has_dn && zl < R) put(W_dn + shift_dn);
+                if (has_up && zl >= nzl - R) put(W_up + shift_up);
+            }
             o += o_step;
             ob += o_step;
             xp += r;
@@ -328,13 +397,20 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
                 ob += o_wrap;
             }
         }
-        cluster_barrier();  // u^{n+1} complete in every strip and ghost row; u^n no longer read
+        if constexpr (AS) {
+            __syncthreads();  // this CTA's rows of u^{n+1} complete, its reads of u^n done
+            if (has_dn) mbar_wait_cl(&mb[0 + (s & 1)], (uint32_t)(s >> 1) & 1u);  // ghost rows of u^{n+1}
+            if (has_up) mbar_wait_cl(&mb[2 + (s & 1)], (uint32_t)(s >> 1) & 1u);
+        } else {
+            cluster_barrier();  // u^{n+1} complete in every strip and ghost row; u^n no longer read
+        }
     };
     for (int s = 0; s < A.nsteps; s += 2) {  // parity unrolled: the level pointers are fixed per call
         step(S0, S1, s);
         if (s + 1 < A.nsteps) step(S1, S0, s + 1);
     }
 
+    if constexpr (AS) cluster_barrier();  // no CTA leaves while a neighbour may still address its memory
     if (A.nsteps > 0 && sp.nrl > 0) {  // the last (partial) chunk of trace rows
         const int s_last = (A.nsteps - 1) / kR2WavRows * kR2WavRows;
         flush_traces(n0 + s_last, A.nsteps - s_last);
@@ -375,7 +451,9 @@ bool r2_choose(const Geom& g, const Sparse& sp, bool damp, R2Plan* out) {
 
 template <int R, bool DAMP>
 cudaError_t r2_launch_k(const R2Args& A, size_t smem, cudaStream_t s) {
-    auto k = resident2d_kernel<R, DAMP>;
+    // AW_R2_SYNC=cluster (development builds): the cluster-barrier variant, for A/B runs
+    static const bool sync_cluster = dev_knob("AW_R2_SYNC") != nullptr;
+    auto k = sync_cluster ? resident2d_kernel<R, DAMP, false> : resident2d_kernel<R, DAMP, true>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
