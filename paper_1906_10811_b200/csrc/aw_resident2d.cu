@@ -106,8 +106,8 @@ R2Plan r2_plan(const Geom& g, const Sparse& sp, bool damp, int CS) {
     o += nent;
     P.o_is = o;
     o += nent;
-    P.o_wav = o;
-    o += sp.nuc > 0 ? kR2WavRows * sp.ns : 0;
+    P.o_wav = o;  // per chunk row, the wavelet value of every injection entry (gathered: q[n][src_e])
+    o += kR2WavRows * nent;
     P.o_tr = o;
     o += kR2WavRows * sp.nrl;
     P.o_mb = (o + 1) / 2 * 2;  // 4 mbarriers (8-byte aligned): ghost rows from below / above, by step parity
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
     const int* iptr = smi + P.o_iptr;
     const int* isrc = smi + P.o_isrc;
     const float* is = smem + P.o_is;
-    float* wav = smem + P.o_wav;     // wavelet rows [s0, s0 + kR2WavRows) of the current chunk
+    float* wav = smem + P.o_wav;     // [row of the chunk][entry]: q[n][src_e] for the chunk's steps
     float* trb = smem + P.o_tr;      // trace rows of the current chunk (written to global once per chunk)
     const Sparse& sp = A.sp;
 
@@ -218,13 +218,34 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
         }
     }
     uint32_t inj_mask = 0;  // bit k: the column pair of unit tid + 1024 k holds an injection corner
+    // this thread's first corners, each packed as (csr begin << 12) | (entries << 6) | (k << 1) | h;
+    // a thread with more than kInjRegs corners finds the rest by binary search
+    constexpr int kInjRegs = 4;
+    int inj_reg[kInjRegs];
+#pragma unroll
+    for (int i = 0; i < kInjRegs; ++i) inj_reg[i] = -1;
+    bool inj_more = false;
     if (sp.nuc > 0) {
+        int nreg = 0;
         for (int c = 0; c < sp.nuc; ++c) {
             const int64_t off = sp.inj_off[c];
             const int zz = (int)(off / A.pitch);
             const int z = zz - R, x = (int)(off - (int64_t)zz * A.pitch);
             const int u = (z - zlo) * A.PR + (x >> 1);
-            if (z >= zlo && z < zlo + nzl && (u & (kR2Threads - 1)) == tid) inj_mask |= 1u << (u / kR2Threads);
+            if (z >= zlo && z < zlo + nzl && (u & (kR2Threads - 1)) == tid) {
+                const int k = u / kR2Threads;
+                inj_mask |= 1u << k;
+                const int e0 = sp.inj_ptr[c], ne = sp.inj_ptr[c + 1] - e0;
+                const int rec = (e0 << 12) | (ne << 6) | (k << 1) | (x & 1);
+                bool placed = false;
+#pragma unroll
+                for (int i = 0; i < kInjRegs; ++i)
+                    if (!placed && i == nreg && ne < 64 && e0 < (1 << 19)) {
+                        inj_reg[i] = rec;
+                        placed = true;
+                    }
+                if (placed) ++nreg; else inj_more = true;
+            }
             if (c % kR2Threads == tid) smi[P.o_ip + c] = z * A.nx + x;
         }
         for (int i = tid; i <= sp.nuc; i += kR2Threads) smi[P.o_iptr + i] = sp.inj_ptr[i];
@@ -281,8 +302,11 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
             // chunk of wavelet rows comes in (the previous one is no longer read)
             if (s > 0) flush_traces(n - kR2WavRows, kR2WavRows);
             const int rows = min(kR2WavRows, A.nsteps - s);
-            if (sp.nuc > 0)
-                for (int i = tid; i < rows * sp.ns; i += kR2Threads) wav[i] = sp.wavelet[n * sp.ns + i];
+            if (sp.nuc > 0)  // gathered: entry e of chunk row rr = q[n + rr][src_e]
+                for (int i = tid; i < rows * sp.nent; i += kR2Threads) {
+                    const int rr = i / sp.nent, e = i - rr * sp.nent;
+                    wav[i] = sp.wavelet[(n + rr) * sp.ns + isrc[e]];
+                }
             __syncthreads();
         }
         // receivers: fma chain over the corners of u^n (before the step), from the last thread down (the
@@ -350,11 +374,21 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
             }
             const int x = 2 * xp;
             if ((inj_mask >> k) & 1u) {
-                // injection corners (CSR order: corner ascending, then source) in this pair: binary search of
-                // the staged corner list per column, then the sequential fma chain over the corner's sources
-                const float* qn = wav + (s % kR2WavRows) * sp.ns;
+                // injection corners of this pair: the sequential fma chain over each corner's sources in CSR
+                // order (corner ascending, then source) -- corners from the registers, and (a thread with more
+                // corners than registers) the rest by binary search of the staged corner list
+                const float* qn = wav + (s % kR2WavRows) * sp.nent;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int i = 0; i < kInjRegs; ++i) {
+                    const int rec = inj_reg[i];
+                    if (rec < 0 || ((rec >> 1) & 31) != k) continue;
+                    const int e0 = rec >> 12, e1 = e0 + ((rec >> 6) & 63);
+                    float v = (rec & 1) ? un.y : un.x;
+                    for (int e = e0; e < e1; ++e) v = __fmaf_rn(is[e], qn[e], v);
+                    if (rec & 1) un.y = v; else un.x = v;
+                }
+#pragma unroll
+                for (int h = 0; h < 2 && inj_more; ++h) {
                     const int pt = (zlo + zl) * A.nx + x + h;
                     int lo = 0, hi = sp.nuc - 1;
                     while (lo < hi) {
@@ -362,8 +396,14 @@ __global__ void __launch_bounds__(kR2Threads, 1) resident2d_kernel(const R2Args 
                         if (ip[mid] < pt) lo = mid + 1; else hi = mid;
                     }
                     if (ip[lo] != pt || x + h >= A.nx) continue;
+                    const int e0 = iptr[lo], e1 = iptr[lo + 1];
+                    bool in_regs = false;  // applied above already
+#pragma unroll
+                    for (int i = 0; i < kInjRegs; ++i)
+                        in_regs |= inj_reg[i] >= 0 && (inj_reg[i] >> 12) == e0 && ((inj_reg[i] >> 1) & 31) == k;
+                    if (in_regs) continue;
                     float v = h ? un.y : un.x;
-                    for (int e = iptr[lo]; e < iptr[lo + 1]; ++e) v = __fmaf_rn(is[e], qn[isrc[e]], v);
+                    for (int e = e0; e < e1; ++e) v = __fmaf_rn(is[e], qn[e], v);
                     if (h) un.y = v; else un.x = v;
                 }
             }

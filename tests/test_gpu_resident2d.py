@@ -110,3 +110,18 @@ def test_resident2d_timing_and_limits(aw):
     ou, oup, orec = orc(w)
     same(u, ou, "u^n")
     same(rec, orec, "traces")
+
+
+def test_resident2d_many_corners_per_thread(aw):
+    # 200 x 200, so 4: strips of 25 rows, 100 column pairs per row, 512 threads per CTA -> thread 0 of
+    # the first CTA owns the pairs of units 0, 512, 1024, ...: sources on those points give it 10 corners,
+    # more than it keeps in registers (the rest go through the binary search of the staged corner list)
+    w = workloads.small_case((200, 200), 4, 18, nbl=6, ns=5, nr=6)
+    h = 10.0
+    w.src_coords = np.array([[h * z, h * x] for z, x in ((0, 0), (5, 24), (10, 48), (15, 72), (20, 96))])
+    (u, up, rec), st = gpu(aw, w, aw.AW_RESIDENT_ON)
+    assert st[-1]["resident"] == 1
+    ou, oup, orec = orc(w)
+    same(u, ou, "u^n")
+    same(up, oup, "u^{n-1}")
+    same(rec, orec, "traces")
