@@ -1520,6 +1520,7 @@ using C6v13 = Cfg<6, 24, 3, 4, 3, 0, 1, true, 0, 40, 0>;   // 8 consumer warps x
 using C6v14 = Cfg<6, 32, 4, 3, 2, 0, 1, true, 0, 40, 0>;   // 8 consumer warps x 4 rows
 // half queue with 4 rows per thread (8 consumer warps, 64 x 32 tiles)
 using C4v6 = Cfg<4, 32, 4, 4, 4, 0, 1, true, 0, 40, 0>;
+using C4v7 = Cfg<4, 32, 4, 4, 4, 0, 1>;   // the round-1 product configuration (8 consumer warps x 4 rows)
 using C5v8 = Cfg<5, 32, 4, 3, 3, 0, 1, true, 0, 40, 0>;
 using C6v15 = Cfg<6, 32, 4, 2, 2, 0, 1, true, 0, 40, 0>;
 using C6v16 = Cfg<6, 32, 4, 3, 1, 0, 1, true, 0, 40, 0>;

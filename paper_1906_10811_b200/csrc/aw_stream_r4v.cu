@@ -10,6 +10,7 @@ const StreamOps* stream_ops_r4_variant(int v) {
         case 4: return ops_of<C4v4>();
         case 5: return ops_of<C4v5>();
         case 6: return ops_of<C4v6>();
+        case 7: return ops_of<C4v7>();
         default: return ops_of<C4v3>();
     }
 }
