@@ -1527,6 +1527,9 @@ using C6v16 = Cfg<6, 32, 4, 3, 1, 0, 1, true, 0, 40, 0>;
 using C7v12 = Cfg<7, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
 using C8v12 = Cfg<8, 32, 4, 2, 1, 0, 1, true, 0, 40, 0>;
 using C8v13 = Cfg<8, 32, 4, 1, 2, 0, 1, true, 0, 40, 0>;
+using C8v15 = Cfg<8, 32, 4, 1, 1, 0, 1, true, 0, 40, 0>;
+using C8v16 = Cfg<8, 24, 4, 3, 2, 0, 1, true, 0, 40, 0>;   // 6 consumer warps x 4 rows
+using C7v13 = Cfg<7, 32, 4, 3, 1, 0, 1, true, 0, 40, 0>;
 // partial queues (z-R .. z+QJ in registers)
 using C8v9 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 2>;
 using C8v10 = Cfg<8, 24, 2, 3, 3, 0, 1, true, 0, 40, 3>;

@@ -10,6 +10,7 @@ const StreamOps* stream_ops_r7() {
     if (variant() == 9) return ops_of<C7v9>();      // partial queue (QJ = 2), 12 consumer warps
     if (variant() == 12) return ops_of<C7v12>();    // half queue, 4 rows per thread
     if (variant() == 10) return ops_of<C7v0>();     // the previous product configuration
+    if (variant() == 13) return ops_of<C7v13>();
 #endif
     return ops_of<C7>();
 }

@@ -17,6 +17,8 @@ const StreamOps* stream_ops_r8_variant(int v) {
         case 12: return ops_of<C8v12>();
         case 13: return ops_of<C8v13>();
         case 14: return ops_of<C8v0>();
+        case 15: return ops_of<C8v15>();
+        case 16: return ops_of<C8v16>();
         default: return ops_of<C8v3>();
     }
 }
