@@ -72,6 +72,18 @@ def test_no_cpu_fallback_without_gpu(aw):
     assert ei.value.status == aw.AW_ECUDA
 
 
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with the CUDA library absent, the first use of the package raises (it never routes
+    to the oracle or to torch ops)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AW_LIBRARY=str(tmp_path / "no_such_libaw.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1906_10811_b200 as aw; aw.Grid"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "no CPU fallback" in r.stderr
+
+
 def test_invalid_arguments_rejected_before_device(aw):
     for shape, so in (((16,), 4), ((16, 16), 3), ((16, 16), 18), ((2, 16), 8)):
         with pytest.raises(aw.AwError) as ei:
